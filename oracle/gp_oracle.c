@@ -274,6 +274,7 @@ static oval eval_rec(const onode* nodes, int64_t* i, const float* X, int64_t ld,
     }
   }
   if (!isfinite(v) || av > (double)FLT_MAX) r.flags |= 1;
+  if (isnan(r.e)) r.e = INFINITY;   /* an undefined first-order bound is "unbounded" */
   return r;
 }
 
@@ -376,7 +377,10 @@ double orc_fitness_sensitivity(int metric, const double* yh, const double* E, co
       if (metric == 0) g = 1.0;
       else if (metric <= 2) g = 2.0 * fabs(d) + E[i];
       else g = fabs(1.0 / (1.0 + exp(-yh[i])) - (double)y[i]) + 0.25 * E[i];
-      s += wi * g * E[i];
+      double c = g * E[i];
+      /* a clamped log-loss row changes by at most the clamp range -ln(1e-15) */
+      if (metric == 3 && !(c <= 34.538776394910684)) c = 34.538776394910684;
+      s += wi * c;
     }
     s /= W;
     if (metric == 2) { /* |sqrt(a) - sqrt(b)| <= min(|a-b| / sqrt(a), sqrt(|a-b|)) */
@@ -412,6 +416,7 @@ double orc_fitness_sensitivity(int metric, const double* yh, const double* E, co
     double g = fabs(((double)y[i] - my) / sqrt(sxx * syy) - r * (yh[i] - mh) / sxx);
     s += wi * g * E[i];
   }
+  if (!(s <= 2.0)) s = 2.0;   /* r lies in [-1, 1] */
   return s;
 }
 

@@ -1,0 +1,476 @@
+// api.cpp -- C-ABI implementation: contexts, gp_evaluate / gp_predict / gp_tournament_select
+// orchestration, the NCCL all-reduce of per-program partial sums, host-pointer staging.
+// Every device step runs in the kernels of aux.cu / eval_s*.cu; this file only validates
+// arguments, sizes workspaces and enqueues work on the context stream.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "gp_internal.h"
+
+using namespace gpb;
+
+// ---------------------------------------------------------------------------------------------
+// NCCL, loaded lazily with dlopen so the library loads (and single-GPU use works) without it.
+// ---------------------------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.tried) {
+    api.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce;
+    }
+  }
+  return api;
+}
+thread_local std::string g_last_global_error;
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// Context helpers
+// ---------------------------------------------------------------------------------------------
+gp_status gp_context::fail(gp_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  err = buf;
+  return s;
+}
+
+gp_status gp_context::cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return GP_OK;
+  return fail(e == cudaErrorMemoryAllocation ? GP_ERR_OOM : GP_ERR_CUDA, "%s: %s", what,
+              cudaGetErrorString(e));
+}
+
+gp_status gp_context::grow(void** p, size_t* cap, size_t bytes, const char* what) {
+  if (*cap >= bytes && *p) return GP_OK;
+  if (*p) cudaFreeAsync(*p, stream);
+  *p = nullptr;
+  *cap = 0;
+  size_t want = std::max(bytes, (size_t)256);
+  want += want / 4;  // amortise growth
+  gp_status s = cuda(cudaMallocAsync(p, want, stream), what);
+  if (s == GP_OK) *cap = want;
+  return s;
+}
+
+bool gpb::is_host_pointer(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+}
+
+// Stages a [host|device] input into a context buffer when it is host memory.
+gp_status gp_context::stage_in(const void* src, size_t bytes, StageBuf& buf, const void** dst,
+                               bool* was_host) {
+  *dst = src;
+  if (!is_host_pointer(src)) return GP_OK;
+  *was_host = true;
+  gp_status s = grow(&buf.p, &buf.cap, bytes, "stage_in");
+  if (s) return s;
+  s = cuda(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, stream), "H2D");
+  *dst = buf.p;
+  return s;
+}
+
+const EvalVariant& gpb::pick_variant(int max_stack) {
+  if (max_stack <= 8) return eval_variant_s8();
+  if (max_stack <= 12) return eval_variant_s12();
+  return eval_variant_s20();
+}
+
+int gpb::sm_count(int device) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  return n > 0 ? n : 148;
+}
+
+// Work decomposition of one evaluator launch: items = row chunk x program
+// group; about 8 waves of items over all resident CTA slots so the hardware block scheduler
+// balances groups of unequal total program length.
+EvalPlan gpb::plan_eval(const EvalVariant& v, int device, int64_t n_rows, int32_t n_programs,
+                        int32_t n_cols, int S, bool predict) {
+  EvalPlan pl;
+  const int tile = v.shape.tile();
+  const int64_t n_tiles = (n_rows + tile - 1) / tile;
+  const int NW = v.shape.NT / 32;
+  const int g_max = 256;
+  // X in shared memory when the tile of all columns fits comfortably.
+  pl.xsmem = (size_t)n_cols * tile * sizeof(float) <= 96 * 1024;
+  auto smem_for = [&](int G) {
+    size_t acc = predict ? 0 : ((((size_t)NW * G * S + NW * 3) * sizeof(double) + 15) & ~(size_t)15);
+    return acc + 2 * (size_t)tile * sizeof(float) +
+           (pl.xsmem ? (size_t)n_cols * tile * sizeof(float) : 0);
+  };
+  int occ = v.occupancy(predict, pl.xsmem, smem_for(g_max));
+  if (occ < 1) occ = 1;
+  const int64_t target = (int64_t)sm_count(device) * occ * 8;
+  const int64_t want_groups = std::max<int64_t>(1, (target + n_tiles - 1) / n_tiles);
+  int G = (int)std::min<int64_t>(g_max, std::max<int64_t>(1, (n_programs + want_groups - 1) / want_groups));
+  const int n_groups = (n_programs + G - 1) / G;
+  int64_t Q = std::min<int64_t>(n_tiles, std::max<int64_t>(1, (target + n_groups - 1) / n_groups));
+  const int64_t tpc = (n_tiles + Q - 1) / Q;
+  Q = (n_tiles + tpc - 1) / tpc;
+  pl.G = G;
+  pl.n_groups = n_groups;
+  pl.n_chunks = Q;
+  pl.rows_per_chunk = tpc * tile;
+  pl.smem = smem_for(G);
+  pl.occupancy = occ;
+  return pl;
+}
+
+// ---------------------------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------------------------
+extern "C" {
+
+const char* gp_status_string(gp_status s) {
+  switch (s) {
+    case GP_OK: return "GP_OK";
+    case GP_ERR_ARG: return "GP_ERR_ARG";
+    case GP_ERR_PROGRAM: return "GP_ERR_PROGRAM";
+    case GP_ERR_UNSUPPORTED: return "GP_ERR_UNSUPPORTED";
+    case GP_ERR_CUDA: return "GP_ERR_CUDA";
+    case GP_ERR_NCCL: return "GP_ERR_NCCL";
+    case GP_ERR_OOM: return "GP_ERR_OOM";
+  }
+  return "GP_ERR_UNKNOWN";
+}
+
+const char* gp_last_error(const gp_context* ctx) {
+  return ctx ? ctx->err.c_str() : g_last_global_error.c_str();
+}
+
+const char* gp_version(void) { return "gp_b200 0.1 sm_100a"; }
+
+gp_status gp_get_unique_id(void* out_id) {
+  if (!out_id) return GP_ERR_ARG;
+  NcclApi& n = nccl();
+  if (!n.ok) { g_last_global_error = "libnccl.so.2 could not be loaded"; return GP_ERR_NCCL; }
+  ncclUniqueId id;
+  ncclResult_t r = n.GetUniqueId(&id);
+  if (r != ncclSuccess) { g_last_global_error = n.GetErrorString(r); return GP_ERR_NCCL; }
+  memcpy(out_id, &id, sizeof id);
+  return GP_OK;
+}
+
+gp_status gp_context_create(gp_context** out, int device, void* stream, const void* nccl_unique_id,
+                            int rank, int world_size) {
+  if (!out || world_size < 1 || rank < 0 || rank >= world_size) return GP_ERR_ARG;
+  *out = nullptr;
+  if (world_size > 1 && !nccl_unique_id) return GP_ERR_ARG;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { g_last_global_error = cudaGetErrorString(e); return GP_ERR_CUDA; }
+  gp_context* c = new gp_context();
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  c->rank = rank;
+  c->world = world_size;
+  c->sms = sm_count(device);
+  if (world_size > 1) {
+    NcclApi& n = nccl();
+    if (!n.ok) { delete c; g_last_global_error = "libnccl.so.2 could not be loaded"; return GP_ERR_NCCL; }
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof id);
+    ncclComm_t comm;
+    ncclResult_t r = n.CommInitRank(&comm, world_size, id, rank);
+    if (r != ncclSuccess) {
+      g_last_global_error = n.GetErrorString(r);
+      delete c;
+      return GP_ERR_NCCL;
+    }
+    c->comm = comm;
+  }
+  *out = c;
+  return GP_OK;
+}
+
+gp_status gp_context_destroy(gp_context* ctx) {
+  if (!ctx) return GP_ERR_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (StageBuf* b : ctx->all_buffers())
+    if (b->p) cudaFree(b->p);
+  for (auto& ev : ctx->ev_pending) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+  for (auto& ev : ctx->ev_free) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
+  if (ctx->comm) nccl().CommDestroy((ncclComm_t)ctx->comm);
+  delete ctx;
+  return GP_OK;
+}
+
+gp_status gp_context_set_stream(gp_context* ctx, void* stream) {
+  if (!ctx) return GP_ERR_ARG;
+  ctx->stream = (cudaStream_t)stream;
+  return GP_OK;
+}
+
+gp_status gp_context_set_profiling(gp_context* ctx, int enabled) {
+  if (!ctx) return GP_ERR_ARG;
+  ctx->profiling = enabled != 0;
+  return GP_OK;
+}
+
+gp_status gp_context_eval_timing(gp_context* ctx, double* total_ms, int64_t* launches, int reset) {
+  if (!ctx) return GP_ERR_ARG;
+  for (auto& ev : ctx->ev_pending) {
+    cudaEventSynchronize(ev.second);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev.first, ev.second);
+    ctx->prof_ms += ms;
+    ctx->prof_launches += 1;
+    ctx->ev_free.push_back(ev);
+  }
+  ctx->ev_pending.clear();
+  if (total_ms) *total_ms = ctx->prof_ms;
+  if (launches) *launches = ctx->prof_launches;
+  if (reset) { ctx->prof_ms = 0.0; ctx->prof_launches = 0; }
+  return GP_OK;
+}
+
+gp_status gp_context_set_reference_row(gp_context* ctx, const float* x_ref, int32_t n_cols,
+                                       float y_ref) {
+  if (!ctx || !x_ref || n_cols < 1) return GP_ERR_ARG;
+  gp_status s = ctx->grow(&ctx->xref.p, &ctx->xref.cap, (size_t)n_cols * sizeof(float) + sizeof(float), "xref");
+  if (s) return s;
+  ctx->xref_host.assign(x_ref, x_ref + n_cols);
+  ctx->xref_host.push_back(y_ref);
+  s = ctx->cuda(cudaMemcpyAsync(ctx->xref.p, ctx->xref_host.data(), ctx->xref_host.size() * sizeof(float),
+                                cudaMemcpyHostToDevice, ctx->stream), "xref H2D");
+  if (s) return s;
+  ctx->xref_cols = n_cols;
+  return ctx->cuda(cudaStreamSynchronize(ctx->stream), "xref sync");
+}
+
+// Shared front half of gp_evaluate / gp_predict: argument checks, staging, compile.
+static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_t*& offsets,
+                         int32_t n_programs, int64_t n_nodes, int32_t max_stack, const float*& X,
+                         int64_t ldx, int64_t n_rows, int32_t n_cols, bool* any_host,
+                         const EvalVariant** var) {
+  if (n_programs < 1 || n_nodes < 1 || max_stack < 1 || max_stack > GP_MAX_STACK || n_rows < 1 ||
+      n_cols < 1 || ldx < n_rows || !programs || !offsets || !X)
+    return ctx->fail(GP_ERR_ARG, "invalid argument (n_programs=%d n_nodes=%lld max_stack=%d "
+                     "n_rows=%lld n_cols=%d ldx=%lld)", n_programs, (long long)n_nodes, max_stack,
+                     (long long)n_rows, n_cols, (long long)ldx);
+  gp_status s;
+  const void* d;
+  if ((s = ctx->stage_in(programs, (size_t)n_nodes * sizeof(gp_node), ctx->h_nodes, &d, any_host))) return s;
+  programs = (const gp_node*)d;
+  if ((s = ctx->stage_in(offsets, (size_t)(n_programs + 1) * sizeof(int64_t), ctx->h_off, &d, any_host))) return s;
+  offsets = (const int64_t*)d;
+  const size_t xbytes = ((size_t)(n_cols - 1) * ldx + n_rows) * sizeof(float);
+  if ((s = ctx->stage_in(X, xbytes, ctx->h_X, &d, any_host))) return s;
+  X = (const float*)d;
+  const EvalVariant& v = pick_variant(max_stack);
+  *var = &v;
+  if ((s = ctx->grow(&ctx->code.p, &ctx->code.cap, (size_t)(n_nodes + 2) * sizeof(uint2), "code"))) return s;
+  if ((s = ctx->grow(&ctx->code_off.p, &ctx->code_off.cap, (size_t)n_programs * sizeof(int64_t), "code_off"))) return s;
+  if ((s = ctx->grow(&ctx->code_len.p, &ctx->code_len.cap, (size_t)n_programs * sizeof(int32_t), "code_len"))) return s;
+  if ((s = ctx->grow(&ctx->status.p, &ctx->status.cap, (size_t)n_programs * sizeof(uint32_t), "status"))) return s;
+  return ctx->cuda(launch_stage(programs, offsets, n_programs, n_nodes, n_cols, v.shape.stack,
+                                (uint2*)ctx->code.p, (int64_t*)ctx->code_off.p,
+                                (int32_t*)ctx->code_len.p, (uint32_t*)ctx->status.p, ctx->stream),
+                   "stage kernel");
+}
+
+gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
+                      int32_t n_programs, int64_t n_nodes, int32_t max_stack, const float* X,
+                      int64_t ldx, const float* y, const float* w, int64_t n_rows, int32_t n_cols,
+                      gp_metric metric, float* fitness_out, uint32_t* status_out) {
+  if (!ctx) return GP_ERR_ARG;
+  cudaSetDevice(ctx->device);
+  if (metric == GP_SPEARMAN)
+    return ctx->fail(GP_ERR_UNSUPPORTED, "Spearman fitness is not on this hot path (SURVEY F1)");
+  if ((int)metric < 0 || (int)metric > GP_PEARSON || !y || !fitness_out)
+    return ctx->fail(GP_ERR_ARG, "invalid metric / y / fitness_out");
+  bool any_host = false;
+  const EvalVariant* v = nullptr;
+  gp_status s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx,
+                        n_rows, n_cols, &any_host, &v);
+  if (s) return s;
+  const void* d;
+  if ((s = ctx->stage_in(y, (size_t)n_rows * sizeof(float), ctx->h_y, &d, &any_host))) return s;
+  y = (const float*)d;
+  if (w) {
+    if ((s = ctx->stage_in(w, (size_t)n_rows * sizeof(float), ctx->h_w, &d, &any_host))) return s;
+    w = (const float*)d;
+  }
+  const bool fit_host = is_host_pointer(fitness_out);
+  const bool st_host = status_out && is_host_pointer(status_out);
+  const int S = metric == GP_PEARSON ? 3 : 1;
+
+  // Pearson reference row and shift (C9)
+  if (metric == GP_PEARSON) {
+    if ((s = ctx->grow(&ctx->shift.p, &ctx->shift.cap, (size_t)n_programs * sizeof(float) + 16, "shift"))) return s;
+    float* shift = (float*)ctx->shift.p;
+    const float* xref;
+    int64_t stride;
+    const float* yref;
+    if (ctx->xref_cols >= n_cols) {
+      xref = (const float*)ctx->xref.p;
+      stride = 1;
+      yref = (const float*)ctx->xref.p + ctx->xref_cols;
+    } else {
+      xref = X;
+      stride = ldx;
+      yref = y;
+    }
+    float* yshift = shift + n_programs;
+    if ((s = ctx->cuda(launch_copy_scalar(yref, yshift, ctx->stream), "y shift"))) return s;
+    if ((s = ctx->cuda(launch_shift((const uint2*)ctx->code.p, (const int64_t*)ctx->code_off.p,
+                                    (const int32_t*)ctx->code_len.p, n_programs, v->shape.stack,
+                                    xref, stride, shift, ctx->stream), "shift kernel"))) return s;
+  }
+
+  // Fused evaluation -> partial sums
+  EvalPlan pl = plan_eval(*v, ctx->device, n_rows, n_programs, n_cols, S, false);
+  const int64_t ld_part = (int64_t)n_programs * S + 3;
+  if ((s = ctx->grow(&ctx->partial.p, &ctx->partial.cap, (size_t)pl.n_chunks * ld_part * sizeof(double), "partial"))) return s;
+  if ((s = ctx->grow(&ctx->sums.p, &ctx->sums.cap, (size_t)ld_part * sizeof(double), "sums"))) return s;
+  EvalArgs a{};
+  a.code = (const uint2*)ctx->code.p;
+  a.code_off = (const int64_t*)ctx->code_off.p;
+  a.code_len = (const int32_t*)ctx->code_len.p;
+  a.X = X;
+  a.ldx = ldx;
+  a.y = y;
+  a.w = w;
+  a.n_rows = n_rows;
+  a.n_cols = n_cols;
+  a.n_programs = n_programs;
+  a.metric = metric;
+  a.G = pl.G;
+  a.rows_per_chunk = pl.rows_per_chunk;
+  a.partial = (double*)ctx->partial.p;
+  a.ld_part = ld_part;
+  a.shift = metric == GP_PEARSON ? (const float*)ctx->shift.p : nullptr;
+  a.y_shift = metric == GP_PEARSON ? (const float*)ctx->shift.p + n_programs : nullptr;
+  ctx->last_plan = pl;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (ctx->profiling) {
+    if (!ctx->ev_free.empty()) { ev = ctx->ev_free.back(); ctx->ev_free.pop_back(); }
+    else { cudaEventCreate(&ev.first); cudaEventCreate(&ev.second); }
+    cudaEventRecord(ev.first, ctx->stream);
+  }
+  if ((s = ctx->cuda(v->launch(a, false, pl.xsmem, dim3((unsigned)pl.n_chunks, (unsigned)pl.n_groups),
+                               pl.smem, ctx->stream), "eval kernel"))) return s;
+  if (ctx->profiling) {
+    cudaEventRecord(ev.second, ctx->stream);
+    ctx->ev_pending.push_back(ev);
+  }
+  if ((s = ctx->cuda(launch_tile_reduce((const double*)ctx->partial.p, pl.n_chunks, ld_part,
+                                        (double*)ctx->sums.p, ctx->stream), "tile_reduce"))) return s;
+  // A6: one all-reduce of the fp64 partial sums across ranks (rows are sharded)
+  if (ctx->world > 1) {
+    NcclApi& n = nccl();
+    ncclResult_t r = n.AllReduce(ctx->sums.p, ctx->sums.p, (size_t)ld_part, ncclFloat64, ncclSum,
+                                 (ncclComm_t)ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return ctx->fail(GP_ERR_NCCL, "ncclAllReduce: %s", n.GetErrorString(r));
+  }
+  // A7: finalize
+  float* fit_dev = fitness_out;
+  if (fit_host) {
+    if ((s = ctx->grow(&ctx->h_fit.p, &ctx->h_fit.cap, (size_t)n_programs * sizeof(float), "fit"))) return s;
+    fit_dev = (float*)ctx->h_fit.p;
+  }
+  if ((s = ctx->cuda(launch_finalize((const double*)ctx->sums.p, n_programs, metric,
+                                     (const int32_t*)ctx->code_len.p, fit_dev,
+                                     (uint32_t*)ctx->status.p, ctx->stream), "finalize"))) return s;
+  if (fit_host) {
+    if ((s = ctx->cuda(cudaMemcpyAsync(fitness_out, fit_dev, (size_t)n_programs * sizeof(float),
+                                       cudaMemcpyDeviceToHost, ctx->stream), "D2H fitness"))) return s;
+  }
+  if (status_out) {
+    if ((s = ctx->cuda(cudaMemcpyAsync(status_out, ctx->status.p, (size_t)n_programs * sizeof(uint32_t),
+                                       st_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                       ctx->stream), "status copy"))) return s;
+  }
+  if (any_host || fit_host || st_host) return ctx->cuda(cudaStreamSynchronize(ctx->stream), "sync");
+  return GP_OK;
+}
+
+gp_status gp_predict(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
+                     int32_t n_programs, int64_t n_nodes, int32_t max_stack, const float* X,
+                     int64_t ldx, int64_t n_rows, int32_t n_cols, float* out, int64_t ld_out,
+                     uint32_t* status_out) {
+  if (!ctx) return GP_ERR_ARG;
+  cudaSetDevice(ctx->device);
+  if (!out || ld_out < n_rows) return ctx->fail(GP_ERR_ARG, "invalid out / ld_out");
+  bool any_host = false;
+  const EvalVariant* v = nullptr;
+  gp_status s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx,
+                        n_rows, n_cols, &any_host, &v);
+  if (s) return s;
+  EvalPlan pl = plan_eval(*v, ctx->device, n_rows, n_programs, n_cols, 1, true);
+  EvalArgs a{};
+  a.code = (const uint2*)ctx->code.p;
+  a.code_off = (const int64_t*)ctx->code_off.p;
+  a.code_len = (const int32_t*)ctx->code_len.p;
+  a.X = X;
+  a.ldx = ldx;
+  a.n_rows = n_rows;
+  a.n_cols = n_cols;
+  a.n_programs = n_programs;
+  a.metric = GP_MSE;
+  a.G = pl.G;
+  a.rows_per_chunk = pl.rows_per_chunk;
+  a.out = out;
+  a.ld_out = ld_out;
+  if ((s = ctx->cuda(v->launch(a, true, pl.xsmem, dim3((unsigned)pl.n_chunks, (unsigned)pl.n_groups),
+                               pl.smem, ctx->stream), "predict kernel"))) return s;
+  if (status_out) {
+    const bool st_host = is_host_pointer(status_out);
+    if ((s = ctx->cuda(cudaMemcpyAsync(status_out, ctx->status.p, (size_t)n_programs * sizeof(uint32_t),
+                                       st_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                       ctx->stream), "status copy"))) return s;
+    if (st_host) any_host = true;
+  }
+  if (any_host) return ctx->cuda(cudaStreamSynchronize(ctx->stream), "sync");
+  return GP_OK;
+}
+
+gp_status gp_tournament_select(gp_context* ctx, const float* fitness, const int64_t* node_offsets,
+                               int32_t n_programs, int32_t n_tournaments, int32_t tournament_size,
+                               float parsimony, int32_t higher_is_better, uint64_t seed,
+                               uint32_t generation, int32_t* winners_out) {
+  if (!ctx) return GP_ERR_ARG;
+  cudaSetDevice(ctx->device);
+  if (!fitness || !node_offsets || !winners_out || n_programs < 1 || n_tournaments < 1 ||
+      tournament_size < 1)
+    return ctx->fail(GP_ERR_ARG, "invalid tournament arguments (n=%d T=%d k=%d)", n_programs,
+                     n_tournaments, tournament_size);
+  return ctx->cuda(launch_select(fitness, node_offsets, n_programs, n_tournaments, tournament_size,
+                                 parsimony, higher_is_better ? 1 : 0, seed, generation,
+                                 winners_out, ctx->stream), "select kernel");
+}
+
+}  // extern "C"

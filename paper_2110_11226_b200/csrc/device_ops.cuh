@@ -1,0 +1,178 @@
+// device_ops.cuh -- fp32 function semantics of the GP catalog on sm_100a.
+//
+// Semantics: SPEC's protected catalog as read in DESIGN.md C2 / include/gp.h.
+// Transcendentals use the SFU (MUFU) approximations: __sinf/__cosf (MUFU.SIN/COS after an
+// FMUL.RZ range scaling), __expf (MUFU.EX2), __logf (MUFU.LG2), rcp.approx (MUFU.RCP); compiled
+// with -ftz=true. Every body is branch-free (selects only).
+// Their error budgets are what the oracle's tolerance model assumes.
+// min/max/clamps follow the oracle's C semantics: fmin/fmax drop a NaN operand, comparison
+// clamps (sinh, asin, acos) propagate it.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/gp.h"
+#include "common.h"
+
+namespace gpb {
+
+constexpr float kProt = 1e-3f;   // S:132 protection threshold, strict "<" (no float in [1e-3, 1e-3f))
+constexpr float kBig = 1e30f;    // S:132 exp clamp; reused for sinh / cosh / pow (C2)
+
+// MUFU.SQRT (no IEEE slow-path call inside the dispatch switch).
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// MUFU.RCP, branch-free (the protected ops select afterwards so no case body contains a branch).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// a = first operand (first popped), b = second operand.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Branch-free bodies for the extended catalog (libdevice versions branch internally, which makes
+// ptxas insert register copies in front of the dispatch for EVERY node). Polynomials: Taylor
+// series where stated, Cephes single-precision minimax coefficients for asin / atan.
+__device__ __forceinline__ float tanh_bf(float a) {
+  const float t = 1.0f - 2.0f * rcp_approx(__expf(2.0f * a) + 1.0f);
+  const float a2 = a * a;
+  const float p = a * (1.0f + a2 * (-1.0f / 3.0f + a2 * (2.0f / 15.0f + a2 * (-17.0f / 315.0f))));
+  return fabsf(a) < 0.125f ? p : t;
+}
+__device__ __forceinline__ float sinh_bf(float a) {
+  const float e = __expf(a), s = 0.5f * (e - rcp_approx(e));
+  const float a2 = a * a;
+  const float p = a * (1.0f + a2 * (1.0f / 6.0f + a2 * (1.0f / 120.0f + a2 * (1.0f / 5040.0f +
+                                                                               a2 / 362880.0f))));
+  const float r = fabsf(a) < 0.5f ? p : s;
+  return r > kBig ? kBig : (r < -kBig ? -kBig : r);
+}
+// asin on [0, 1] given z and s (Cephes asinf): |x| <= 0.5: s = |x|, z = x^2;
+// |x| > 0.5: z = (1 - |x|) / 2, s = sqrt(z), asin|x| = pi/2 - 2 * core.
+__device__ __forceinline__ float asin_core(float s, float z) {
+  const float p = (((4.2163199048e-2f * z + 2.4181311049e-2f) * z + 4.5470025998e-2f) * z +
+                   7.4953002686e-2f) * z + 1.6666752422e-1f;
+  return s + s * z * p;
+}
+__device__ __forceinline__ float asin_bf(float x) {
+  x = x < -1.0f ? -1.0f : (x > 1.0f ? 1.0f : x);
+  const float ax = fabsf(x);
+  const bool big = ax > 0.5f;
+  const float z = big ? 0.5f * (1.0f - ax) : ax * ax;
+  const float c = asin_core(big ? sqrt_approx(z) : ax, z);
+  return copysignf(big ? 1.57079632679489662f - 2.0f * c : c, x);
+}
+__device__ __forceinline__ float acos_bf(float x) {
+  x = x < -1.0f ? -1.0f : (x > 1.0f ? 1.0f : x);
+  const float ax = fabsf(x);
+  const bool big = ax > 0.5f;
+  const float z = big ? 0.5f * (1.0f - ax) : ax * ax;
+  const float c = asin_core(big ? sqrt_approx(z) : ax, z);
+  const float small_r = 1.57079632679489662f - copysignf(c, x);
+  const float big_r = x > 0.0f ? 2.0f * c : 3.14159265358979324f - 2.0f * c;
+  return big ? big_r : small_r;
+}
+__device__ __forceinline__ float atan_bf(float x) {
+  const float ax = fabsf(x);
+  const bool c1 = ax > 2.414213562373095f, c2 = ax > 0.4142135623730950f;  // tan(3pi/8), tan(pi/8)
+  const float xr = c1 ? -rcp_approx(ax) : (c2 ? (ax - 1.0f) * rcp_approx(ax + 1.0f) : ax);
+  const float y0 = c1 ? 1.57079632679489662f : (c2 ? 0.78539816339744831f : 0.0f);
+  const float z = xr * xr;
+  const float r = y0 + ((((8.05374449538e-2f * z - 1.38776856032e-1f) * z + 1.99777106478e-1f) * z -
+                         3.33329491539e-1f) * z * xr + xr);
+  return copysignf(r, x);
+}
+
+// a = first operand (first popped), b = second operand.
+template <int OP>
+__device__ __forceinline__ float apply2(float a, float b) {
+  if constexpr (OP == GP_OP_ADD) return a + b;
+  else if constexpr (OP == GP_OP_SUB) return a - b;
+  else if constexpr (OP == GP_OP_MUL) return a * b;
+  else if constexpr (OP == GP_OP_DIV) { const float q = a * rcp_approx(b); return fabsf(b) < kProt ? 1.0f : q; }
+  else if constexpr (OP == GP_OP_MIN) return fminf(a, b);
+  else if constexpr (OP == GP_OP_MAX) return fmaxf(a, b);
+  else {  // GP_OP_POW: |a|^b = 2^(b * log2|a|), clamped; 0^b and b == 0 by selects
+    const float r = fminf(ex2_approx(b * lg2_approx(fabsf(a))), kBig);
+    const float r0 = a == 0.0f ? (b > 0.0f ? 0.0f : kBig) : r;
+    return b == 0.0f ? 1.0f : r0;
+  }
+}
+
+template <int OP>
+__device__ __forceinline__ float apply1(float a) {
+  if constexpr (OP == GP_OP_SIN) return __sinf(a);
+  else if constexpr (OP == GP_OP_COS) return __cosf(a);
+  else if constexpr (OP == GP_OP_TAN) return __sinf(a) * rcp_approx(__cosf(a));
+  else if constexpr (OP == GP_OP_ABS) return fabsf(a);
+  else if constexpr (OP == GP_OP_NEG) return -a;
+  else if constexpr (OP == GP_OP_SQRT) return sqrt_approx(fabsf(a));
+  else if constexpr (OP == GP_OP_LOG) { const float l = __logf(fabsf(a)); return fabsf(a) < kProt ? 0.0f : l; }
+  else if constexpr (OP == GP_OP_EXP) return fminf(__expf(a), kBig);
+  else if constexpr (OP == GP_OP_INV) { const float r = rcp_approx(a); return fabsf(a) < kProt ? 1.0f : r; }
+  else if constexpr (OP == GP_OP_SQUARE) return a * a;
+  else if constexpr (OP == GP_OP_CUBE) return a * a * a;
+  else if constexpr (OP == GP_OP_TANH) return tanh_bf(a);
+  else if constexpr (OP == GP_OP_SINH) return sinh_bf(a);
+  else if constexpr (OP == GP_OP_COSH) { const float e = __expf(fabsf(a)); return fminf(0.5f * (e + rcp_approx(e)), kBig); }
+  else if constexpr (OP == GP_OP_ASIN) return asin_bf(a);
+  else if constexpr (OP == GP_OP_ACOS) return acos_bf(a);
+  else return atan_bf(a);  // GP_OP_ATAN
+}
+
+// Runtime-dispatched scalar version (used by the Pearson shift kernel: one row per program).
+__device__ __forceinline__ float apply_rt(int op, float a, float b) {
+  switch (op) {
+    case GP_OP_ADD: return apply2<GP_OP_ADD>(a, b);
+    case GP_OP_SUB: return apply2<GP_OP_SUB>(a, b);
+    case GP_OP_MUL: return apply2<GP_OP_MUL>(a, b);
+    case GP_OP_DIV: return apply2<GP_OP_DIV>(a, b);
+    case GP_OP_MIN: return apply2<GP_OP_MIN>(a, b);
+    case GP_OP_MAX: return apply2<GP_OP_MAX>(a, b);
+    case GP_OP_POW: return apply2<GP_OP_POW>(a, b);
+    case GP_OP_SIN: return apply1<GP_OP_SIN>(a);
+    case GP_OP_COS: return apply1<GP_OP_COS>(a);
+    case GP_OP_TAN: return apply1<GP_OP_TAN>(a);
+    case GP_OP_ABS: return apply1<GP_OP_ABS>(a);
+    case GP_OP_NEG: return apply1<GP_OP_NEG>(a);
+    case GP_OP_SQRT: return apply1<GP_OP_SQRT>(a);
+    case GP_OP_LOG: return apply1<GP_OP_LOG>(a);
+    case GP_OP_EXP: return apply1<GP_OP_EXP>(a);
+    case GP_OP_INV: return apply1<GP_OP_INV>(a);
+    case GP_OP_SQUARE: return apply1<GP_OP_SQUARE>(a);
+    case GP_OP_CUBE: return apply1<GP_OP_CUBE>(a);
+    case GP_OP_TANH: return apply1<GP_OP_TANH>(a);
+    case GP_OP_SINH: return apply1<GP_OP_SINH>(a);
+    case GP_OP_COSH: return apply1<GP_OP_COSH>(a);
+    case GP_OP_ASIN: return apply1<GP_OP_ASIN>(a);
+    case GP_OP_ACOS: return apply1<GP_OP_ACOS>(a);
+    case GP_OP_ATAN: return apply1<GP_OP_ATAN>(a);
+  }
+  return __int_as_float(0x7fc00000);
+}
+
+// ---- compiled program word (written by the stage kernel, read by the evaluator) ---------------
+// One uint2 per node, stored in EVALUATION order (reverse prefix):
+//   .x bits [0,10)  : case id = kind * STACK + slot, kind = op (0 var, 1 const, 2.. functions)
+//       bits [10,32): variable index (var nodes)
+//   .y              : fp32 constant bits (const nodes)
+// slot = destination stack slot, static per node (the occupancy before/after each node depends
+// only on the tree shape, never on data): terminal -> sp, unary -> sp-1, binary -> sp-2.
+constexpr int kCaseBits = 10;
+constexpr uint32_t kCaseMask = (1u << kCaseBits) - 1u;
+
+}  // namespace gpb

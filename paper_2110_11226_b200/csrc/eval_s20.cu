@@ -1,0 +1,6 @@
+// Evaluator variant: register stack of 20 slots, 4 rows per thread per pass, 4 passes per tile.
+#define GP_STACK 20
+#define GP_R 4
+#define GP_SUB 4
+#define GP_NT 128
+#include "eval_impl.cuh"

@@ -1,0 +1,6 @@
+// Evaluator variant: register stack of 8 slots, 8 rows per thread per pass, 2 passes per tile.
+#define GP_STACK 8
+#define GP_R 8
+#define GP_SUB 2
+#define GP_NT 128
+#include "eval_impl.cuh"

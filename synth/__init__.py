@@ -104,6 +104,48 @@ def random_population(n: int, seed: int = 1, depth=(1, 6), funcs=TABLE2_SET, n_f
     return flatten(progs)
 
 
+def deep_population(n: int, seed: int = 1, need=(9, 20), funcs=(2, 3, 4, 9, 10),
+                    n_features: int = 2, const_range=(-1.0, 1.0)):
+    """Left-deep programs with a prescribed reverse-prefix stack need in [need[0], need[1]]: each
+    binary node's FIRST operand carries the deep chain (the second operand is evaluated first and
+    stays on the stack), so a chain of d binary nodes needs d + 1 slots. Sides are terminals or
+    unary-wrapped terminals; sin/cos in the default op mix keep values bounded (well-conditioned
+    programs for exercising every stack slot of the 12- and 20-slot kernels)."""
+    rng = np.random.default_rng(seed)
+    binary = [f for f in funcs if f in BINARY]
+    unary = [f for f in funcs if f in UNARY]
+
+    def term():
+        if rng.random() < 0.5:
+            return [(VAR, int(rng.integers(n_features)))]
+        v = np.float32(rng.uniform(*const_range))
+        return [(CONST, int(np.array([v]).view(np.int32)[0]))]
+
+    progs = []
+    for _ in range(n):
+        d = int(rng.integers(need[0], need[1] + 1)) - 1
+        out = []
+        for _ in range(d):
+            if unary and rng.random() < 0.3:
+                out.append((int(rng.choice(unary)), 0))
+            out.append((int(rng.choice(binary)), 0))
+        out += term()
+        # prefix = b_1 [u] b_2 [u] ... b_d t0 s_d ... s_1: the second operand s_i of b_i follows
+        # b_i's first-operand chain; each s_i is a terminal or a unary of a terminal
+        seconds = []
+        for op, _ in out:
+            if op in BINARY:
+                s = term()
+                if unary and rng.random() < 0.5:
+                    s = [(int(rng.choice(unary)), 0)] + s
+                seconds.append(s)
+        prog = list(out)
+        for s in reversed(seconds):
+            prog += s
+        progs.append(prog)
+    return flatten(progs)
+
+
 def stack_occupancy(prog) -> int:
     """Maximum occupancy of a reverse-prefix stack walk (counter only; for input filtering)."""
     sp = need = 0

@@ -1,0 +1,95 @@
+"""GPU engine (gp_generation) against the oracle's replay of Alg. 1, and full-size sampled parity.
+
+Teacher forcing: each generation the oracle selects and mutates from the SAME fp32 fitness the GPU
+produced, so kinds, tournament winners and children must be bit-identical; the GPU fitness of the
+children is checked against the oracle's evaluation within the tolerance model."""
+import numpy as np
+import pytest
+
+import synth
+from tests.test_gpu_parity import check_fitness, dev
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gp():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2110_11226_b200 as gp
+    return gp
+
+
+@pytest.fixture(scope="module")
+def ctx(gp):
+    c = gp.Context(0)
+    yield c
+    c.close()
+
+
+def _oracle_cfg(oe, **kw):
+    return oe.Config(**kw)
+
+
+@pytest.mark.parametrize("metric", ["mse", "pearson"])
+def test_engine_teacher_forced_replay_c1(gp, ctx, orc, metric):
+    """C1 (BASELINE configs[0]): Pagie 64x64, population 256, 10 generations (incl. gen 0)."""
+    from oracle import engine as oe
+    X, y = synth.pagie_grid(64)
+    e = gp.Engine(ctx, dev(X), dev(y), population_size=256, metric=metric, seed=2110)
+    ocfg = oe.Config(population_size=256, metric=metric, seed=2110)
+    e.init_population()
+    nodes, off, fit = e.population()
+    opop = oe.ramped_init(ocfg)
+    on, oo = oe.flatten(opop)
+    assert np.array_equal(nodes, on) and np.array_equal(off, oo)
+    ref, sens, flags = orc.population_fitness(nodes, off, X, y, None, metric)
+    check_fitness(fit, ref, sens, flags, metric)
+    hb = metric == "pearson"
+    for g in range(1, 10):
+        st = e.generation()
+        kinds, winners = e.last_selection()
+        rec = oe.next_generation(opop, fit, ocfg, g, hb)
+        assert kinds.tolist() == rec.kinds
+        assert np.array_equal(winners, rec.winners)
+        nodes, off, fit = e.population()
+        on, oo = oe.flatten(rec.population)
+        assert np.array_equal(off, oo) and np.array_equal(nodes, on), f"generation {g}"
+        ref, sens, flags = orc.population_fitness(nodes, off, X, y, None, metric)
+        check_fitness(fit, ref, sens, flags, metric)
+        assert st["generation"] == g and st["n_tournaments"] == len(winners)
+        opop = rec.population
+
+
+def test_engine_thread_count_independent(gp, ctx):
+    X, y = synth.pagie_grid(32)
+    outs = []
+    for threads in (1, 7):
+        e = gp.Engine(ctx, dev(X), dev(y), population_size=300, metric="mae", seed=5,
+                      n_threads=threads)
+        e.init_population()
+        for _ in range(3):
+            e.generation()
+        outs.append(e.population())
+        e.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_full_size_c3_sampled(gp, ctx, orc):
+    """C3 at full size in the bench launch configuration (16,777,216 rows x 8192 programs):
+    sampled programs' fitness against the oracle over ALL rows."""
+    X, y = synth.pagie_grid(4096)
+    e = gp.Engine(ctx, dev(X), dev(y), population_size=8192, metric="mse", seed=2110)
+    e.init_population()
+    e.generation()
+    nodes, off, fit = e.population()
+    rng = np.random.default_rng(0)
+    lens = np.diff(off)
+    sample = list(rng.choice(np.where(lens > 5)[0], 3, replace=False)) + [int(np.argmax(lens))]
+    sub_nodes = np.concatenate([nodes[off[p]:off[p + 1]] for p in sample])
+    sub_off = np.zeros(len(sample) + 1, np.int64)
+    sub_off[1:] = np.cumsum([lens[p] for p in sample])
+    ref, sens, flags = orc.population_fitness(sub_nodes, sub_off, X, y, None, "mse")
+    check_fitness(fit[sample], ref, sens, flags, "mse", max_excluded=1.0)

@@ -1,0 +1,280 @@
+"""GPU parity: the sm_100a path (through the C-ABI binding) against the CPU oracle.
+
+Tolerances: per row |gpu - ref| <= max(1e-4 |ref|, 1e-6, 4 E) with E
+the oracle's propagated fp32 error bound; per program |F_gpu - F_ref| <= 1e-4 max(|F_ref|, floor)
++ 4 * sensitivity (sum_i |dF/dyhat_i| E_i). Rows / programs the oracle flags as fp32-overflow or
+protected-branch-ambiguous are excluded and counted (they must stay rare).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+F_OVF, F_AMB, F_INV, F_UND = 1, 2, 4, 8
+# Tolerance model: DESIGN.md "Tolerance model" (north_star: relative 1e-4 in fp32).
+
+
+@pytest.fixture(scope="module")
+def gp():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2110_11226_b200 as gp
+    gp.lib()
+    return gp
+
+
+@pytest.fixture(scope="module")
+def ctx(gp):
+    c = gp.Context(0)
+    yield c
+    c.close()
+
+
+def dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def check_rows(orc, nodes, off, X, gpu_out):
+    """Row-level parity of gp_predict; returns (checked, skipped)."""
+    checked = skipped = 0
+    for p in range(len(off) - 1):
+        v, e, fl = orc.eval_program(nodes[off[p]:off[p + 1]], X)
+        g = gpu_out[p]
+        bad = (fl != 0) | (np.abs(v) + 4 * e > 3e38) | ~np.isfinite(e)
+        ok = bad | (np.abs(g - v) <= np.maximum(np.maximum(1e-4 * np.abs(v), 1e-6), 4 * e)) | \
+            (np.isnan(g) & np.isnan(v))
+        if not ok.all():
+            i = int(np.argmin(ok))
+            raise AssertionError(f"program {p} row {i}: gpu {g[i]!r} ref {v[i]!r} E {e[i]!r} "
+                                 f"prog {nodes[off[p]:off[p + 1]].tolist()}")
+        checked += int((~bad).sum())
+        skipped += int(bad.sum())
+    return checked, skipped
+
+
+def check_fitness(gpu_fit, ref, sens, flags, metric, max_excluded=0.03):
+    # Pearson r lies in [-1, 1]: fp32 accumulation over >= 1e3 rows gives absolute errors of
+    # order 1e-8 independent of |r|, so its floor is absolute (1e-4 * 1e-2 = 1e-6 on r).
+    floor = 1e-2 if metric == "pearson" else 1e-6
+    excluded = 0
+    for p in range(len(ref)):
+        if flags[p] & F_INV:
+            assert gpu_fit[p] == (-math.inf if metric == "pearson" else math.inf), p
+            continue
+        r, g = ref[p], float(gpu_fit[p])
+        if flags[p] & F_UND and not flags[p] & (F_OVF | F_AMB):
+            assert g == 0.0, (p, g)          # constant program: Pearson undefined -> 0 (C4)
+            continue
+        if flags[p] & (F_OVF | F_AMB) or not math.isfinite(sens[p]):
+            excluded += 1                    # no usable error bound: reported, not compared
+            continue
+        if math.isinf(r):
+            assert math.isinf(g), (p, g, r)
+            continue
+        tol = 1e-4 * max(abs(r), floor) + 4 * sens[p] + abs(r) * 2 ** -23
+        assert abs(g - r) <= tol, f"program {p}: gpu {g!r} ref {r!r} tol {tol!r} sens {sens[p]!r}"
+    assert excluded <= max_excluded * len(ref) + 1, excluded
+
+
+# ---- execution step (gp_predict) ---------------------------------------------------------------
+@pytest.mark.parametrize("funcs,max_stack,depth", [
+    (synth.TABLE2_SET, 8, (1, 6)),
+    (synth.ALL_FUNCS, 8, (1, 6)),
+])
+def test_predict_rows_match_oracle(gp, ctx, orc, funcs, max_stack, depth):
+    nodes, off = synth.random_population(120, seed=max_stack + len(funcs), depth=depth,
+                                         funcs=funcs, max_stack=max_stack, p_terminal=0.25)
+    X, _ = synth.pagie_grid(48)            # 2304 rows: one full tile + ragged tail (s8 tile 2048)
+    out, st = ctx.predict(dev(nodes), dev(off), dev(X), max_stack=max_stack)
+    torch.cuda.synchronize()
+    assert (st.cpu().numpy() == 0).all()
+    checked, skipped = check_rows(orc, nodes, off, X, out.cpu().numpy())
+    assert skipped <= 0.02 * (checked + skipped)
+
+
+@pytest.mark.parametrize("max_stack", [12, 20])
+def test_predict_every_stack_slot(gp, ctx, orc, max_stack):
+    """Left-deep programs whose stack need spans 1..max_stack exercise every (op, slot) case of
+    the 12- and 20-slot kernels; plus shallow random programs through the same kernel."""
+    dn, do = synth.deep_population(60, seed=max_stack, need=(2, max_stack))
+    rn, ro = synth.random_population(40, seed=3, depth=(1, 6), max_stack=8)
+    nodes = np.concatenate([dn, rn])
+    off = np.concatenate([do, ro[1:] + do[-1]])
+    X, _ = synth.pagie_grid(40)
+    out, st = ctx.predict(dev(nodes), dev(off), dev(X), max_stack=max_stack)
+    assert (st.cpu().numpy() == 0).all()
+    checked, skipped = check_rows(orc, nodes, off, X, out.cpu().numpy())
+    assert skipped <= 0.02 * (checked + skipped)
+
+
+def test_predict_deep_random_all_ops_stress(gp, ctx, orc):
+    """Random depth-8..19 programs over the whole catalog through the 20-slot kernel. Many such
+    programs are ill-conditioned in fp32 (their error bound is unbounded); the rest must match."""
+    nodes, off = synth.random_population(120, seed=23, depth=(8, 19), funcs=synth.ALL_FUNCS,
+                                         max_stack=20, p_terminal=0.25)
+    X, _ = synth.pagie_grid(40)
+    out, st = ctx.predict(dev(nodes), dev(off), dev(X), max_stack=20)
+    checked, skipped = check_rows(orc, nodes, off, X, out.cpu().numpy())
+    assert checked >= 0.6 * (checked + skipped)
+
+
+def test_predict_global_x_path(gp, ctx, orc):
+    # 28 columns x 2048-row tile exceeds the shared-memory X budget -> per-node L1/L2 loads
+    X, _ = synth.higgs_like(2048 * 2 + 301, seed=4)
+    nodes, off = synth.random_population(60, seed=9, depth=(1, 6), funcs=synth.ALL_FUNCS,
+                                         n_features=28, max_stack=8)
+    out, st = ctx.predict(dev(nodes), dev(off), dev(X), max_stack=8)
+    torch.cuda.synchronize()
+    check_rows(orc, nodes, off, X, out.cpu().numpy())
+
+
+def test_pagie_program_exact(gp, ctx, orc):
+    from tests.test_oracle_structure_eval import pagie_program
+    p = pagie_program(orc)
+    off = np.array([0, len(p)], np.int64)
+    X, y = synth.pagie_grid(64)
+    out, st = ctx.predict(dev(p), dev(off), dev(X), max_stack=8)
+    g = out.cpu().numpy()[0]
+    assert np.max(np.abs(g - y)) < 1e-6
+    fit, _ = ctx.evaluate(dev(p), dev(off), dev(X), dev(y), metric="mse", max_stack=8)
+    assert float(fit.cpu()[0]) < 1e-12
+
+
+# ---- fused evaluation + fitness (gp_evaluate) ----------------------------------------------------
+def _dataset(metric, n_rows, seed=0):
+    if metric == "logloss":
+        X, y = synth.higgs_like(n_rows, seed=seed, n_cols=3)
+    else:
+        side = int(math.isqrt(n_rows))
+        X, y = synth.pagie_grid(side)
+        X, y = X[:, :n_rows], y[:n_rows]
+    return np.ascontiguousarray(X), np.ascontiguousarray(y)
+
+
+@pytest.mark.parametrize("metric", ["mae", "mse", "rmse", "logloss", "pearson"])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_evaluate_fitness_matches_oracle(gp, ctx, orc, metric, weighted):
+    n_rows = 3 * 2048 + 37                  # several tiles + ragged tail
+    X, y = _dataset(metric, n_rows, seed=3)
+    n_feat = X.shape[0]
+    nodes, off = synth.random_population(160, seed=100 + len(metric), depth=(0, 6),
+                                         n_features=n_feat, max_stack=8)
+    w = synth.weights(n_rows, seed=5) if weighted else None
+    fit, st = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), None if w is None else dev(w),
+                           metric=metric, max_stack=8)
+    torch.cuda.synchronize()
+    ref, sens, flags = orc.population_fitness(nodes, off, X, y, w, metric)
+    check_fitness(fit.cpu().numpy(), ref, sens, flags, metric)
+
+
+@pytest.mark.parametrize("max_stack", [12, 20])
+@pytest.mark.parametrize("metric", ["mse", "pearson"])
+def test_evaluate_deep_variants(gp, ctx, orc, max_stack, metric):
+    X, y = synth.pagie_grid(40)
+    nodes, off = synth.deep_population(80, seed=max_stack, need=(2, max_stack))
+    fit, st = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric=metric,
+                           max_stack=max_stack)
+    ref, sens, flags = orc.population_fitness(nodes, off, X, y, None, metric)
+    check_fitness(fit.cpu().numpy(), ref, sens, flags, metric)
+
+
+def test_evaluate_global_x_path_logloss(gp, ctx, orc):
+    X, y = synth.higgs_like(2048 * 3 + 5, seed=12)          # 28 columns -> global X path
+    nodes, off = synth.random_population(60, seed=13, depth=(1, 6), n_features=28, max_stack=8)
+    w = synth.weights(X.shape[1], seed=2)
+    fit, _ = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), dev(w), metric="logloss",
+                          max_stack=8)
+    ref, sens, flags = orc.population_fitness(nodes, off, X, y, w, "logloss")
+    check_fitness(fit.cpu().numpy(), ref, sens, flags, "logloss")
+
+
+def test_host_pointers_match_device(gp, ctx, orc):
+    X, y = synth.pagie_grid(30)
+    nodes, off = synth.random_population(50, seed=77, depth=(1, 5), max_stack=8)
+    f_dev, s_dev = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="mse", max_stack=8)
+    fh = torch.empty(50, dtype=torch.float32)
+    sh = torch.empty(50, dtype=torch.int32)
+    ctx.evaluate(nodes, off, X, y, metric="mse", max_stack=8, fitness_out=fh, status_out=sh)
+    assert torch.equal(f_dev.cpu(), fh) and torch.equal(s_dev.cpu(), sh)
+
+
+def test_determinism(gp, ctx):
+    X, y = synth.pagie_grid(100)
+    nodes, off = synth.random_population(300, seed=5, depth=(1, 6), max_stack=8)
+    a, _ = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="pearson", max_stack=8)
+    b, _ = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="pearson", max_stack=8)
+    assert torch.equal(a, b)
+
+
+# ---- edge cases --------------------------------------------------------------------------------
+def test_edge_cases(gp, ctx, orc):
+    P = orc.program
+    progs = [
+        P(("var", 1)),                                          # length 1
+        P(("const", 0.25)),                                     # constant: Pearson undefined
+        P("add", ("var", 0)),                                   # dangling -> invalid
+        P(("var", 0), ("var", 1)),                              # underflow -> invalid
+        P(("var", 5)),                                          # var out of range
+        P("add", "add", "add", "add", "add", "add", "add", "add", *([("var", 0)] * 9)),  # need 9
+        P("div", ("var", 0), "sub", ("var", 1), ("var", 1)),    # protected division by 0
+    ]
+    nodes = np.concatenate(progs)
+    off = np.zeros(len(progs) + 1, np.int64)
+    off[1:] = np.cumsum([len(p) for p in progs])
+    X, y = synth.pagie_grid(9)
+    fit, st = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="mse", max_stack=8)
+    fit, st = fit.cpu().numpy(), st.cpu().numpy()
+    assert st[0] == 0 and st[1] == 0 and st[6] == 0
+    assert st[2] & 1 and st[3] & 1 and st[4] & 4 and st[5] & 2
+    assert np.isinf(fit[2:6]).all()
+    ref, sens, fl = orc.population_fitness(nodes, off, X, y, None, "mse")
+    for p in (0, 1, 6):
+        assert abs(fit[p] - ref[p]) <= 1e-4 * abs(ref[p]) + 1e-6
+    fitp, stp = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="pearson", max_stack=8)
+    assert fitp.cpu().numpy()[1] == 0.0 and stp.cpu().numpy()[1] & 16
+    # one row, one program
+    f1, _ = ctx.evaluate(dev(progs[0]), dev(np.array([0, 1], np.int64)), dev(X[:, :1]),
+                         dev(y[:1]), metric="mae", max_stack=8)
+    assert abs(float(f1.cpu()[0]) - abs(X[1, 0] - y[0])) < 1e-6
+    # zero-weight rows never contaminate, even when the loss there is inf
+    w = np.ones(X.shape[1], np.float32)
+    w[::2] = 0
+    fw, _ = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), dev(w), metric="mse", max_stack=8)
+    rw, _, _ = orc.population_fitness(nodes, off, X, y, w, "mse")
+    assert abs(fw.cpu().numpy()[0] - rw[0]) <= 1e-4 * rw[0]
+    with pytest.raises(gp.GPError):
+        ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="spearman", max_stack=8)
+
+
+# ---- tournament selection: bit-exact against the oracle replay --------------------------------------
+@pytest.mark.parametrize("k", [1, 2, 4, 7, 20])
+def test_tournament_bit_exact(gp, ctx, orc, k):
+    rng = np.random.default_rng(k)
+    n = 1000
+    fit = rng.integers(0, 50, n).astype(np.float32) / 7          # ties
+    fit[rng.random(n) < 0.05] = np.nan
+    lens = rng.integers(1, 40, n)
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    for hb in (False, True):
+        w = ctx.tournament_select(dev(fit), dev(off), 5000, k, 0.01, hb, seed=12345 + k,
+                                  generation=3)
+        ref = orc.tournament(fit, lens.astype(np.int32), 5000, k, 0.01, hb, 12345 + k, 3)
+        assert np.array_equal(w.cpu().numpy(), ref)
+
+
+def test_tournament_win_law(gp, ctx):
+    fit = np.array([0.5, 0.1, 0.9], np.float32)
+    off = np.array([0, 1, 2, 3], np.int64)
+    w = ctx.tournament_select(dev(fit), dev(off), 1_000_000, 2, 0.0, False, seed=1, generation=1)
+    cnt = np.bincount(w.cpu().numpy(), minlength=3)
+    expect = 1e6 * np.array([3 / 9, 5 / 9, 1 / 9])
+    assert ((cnt - expect) ** 2 / expect).sum() < 13.8
