@@ -102,40 +102,27 @@ gp_status gp_context::stage_in(const void* src, size_t bytes, StageBuf& buf, con
   return s;
 }
 
-const EvalVariant& gpb::pick_variant(int max_stack) {
-  if (max_stack <= 8) return eval_variant_s8();
-  if (max_stack <= 12) return eval_variant_s12();
-  return eval_variant_s20();
-}
-
 int gpb::sm_count(int device) {
   int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
   return n > 0 ? n : 148;
 }
 
-// Work decomposition of one evaluator launch: items = row chunk x program
-// group; about 8 waves of items over all resident CTA slots so the hardware block scheduler
-// balances groups of unequal total program length.
-EvalPlan gpb::plan_eval(const EvalVariant& v, int device, int64_t n_rows, int32_t n_programs,
-                        int32_t n_cols, int S, bool predict) {
+// Work decomposition shared by every variant launch: items = program group x
+// row chunk, about 8 items per resident CTA slot so the persistent CTAs' queue balances groups
+// of unequal total program length. All variants share the 2048-row tile.
+EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t n_cols, int S,
+                        bool predict) {
   EvalPlan pl;
-  const int tile = v.shape.tile();
+  const int tile = kTile;
   const int64_t n_tiles = (n_rows + tile - 1) / tile;
-  const int NW = v.shape.NT / 32;
+  const int NW = 4;  // NT = 128 in every variant
   const int g_max = 256;
-  // X in shared memory when the tile of all columns fits comfortably.
   pl.xsmem = (size_t)n_cols * tile * sizeof(float) <= 96 * 1024;
-  auto smem_for = [&](int G) {
-    size_t acc = predict ? 0 : ((((size_t)NW * G * S + NW * 3) * sizeof(double) + 15) & ~(size_t)15);
-    return acc + 2 * (size_t)tile * sizeof(float) +
-           (pl.xsmem ? (size_t)n_cols * tile * sizeof(float) : 0);
-  };
-  int occ = v.occupancy(predict, pl.xsmem, smem_for(g_max));
-  if (occ < 1) occ = 1;
-  const int64_t target = (int64_t)sm_count(device) * occ * 8;
+  const int occ_guess = 4;
+  const int64_t target = (int64_t)sm_count(device) * occ_guess * 8;
   const int64_t want_groups = std::max<int64_t>(1, (target + n_tiles - 1) / n_tiles);
-  int G = (int)std::min<int64_t>(g_max, std::max<int64_t>(1, (n_programs + want_groups - 1) / want_groups));
+  const int G = (int)std::min<int64_t>(g_max, std::max<int64_t>(1, (n_programs + want_groups - 1) / want_groups));
   const int n_groups = (n_programs + G - 1) / G;
   int64_t Q = std::min<int64_t>(n_tiles, std::max<int64_t>(1, (target + n_groups - 1) / n_groups));
   const int64_t tpc = (n_tiles + Q - 1) / Q;
@@ -144,9 +131,49 @@ EvalPlan gpb::plan_eval(const EvalVariant& v, int device, int64_t n_rows, int32_
   pl.n_groups = n_groups;
   pl.n_chunks = Q;
   pl.rows_per_chunk = tpc * tile;
-  pl.smem = smem_for(G);
-  pl.occupancy = occ;
+  const size_t acc = predict ? 0 : (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15);
+  pl.smem = acc + 2 * (size_t)tile * sizeof(float) + (pl.xsmem ? (size_t)n_cols * tile * sizeof(float) : 0);
   return pl;
+}
+
+static const EvalVariant& variant(int v) {
+  switch (v) {
+    case 0: return eval_variant_s4();
+    case 1: return eval_variant_s8();
+    case 2: return eval_variant_s12();
+    default: return eval_variant_s20();
+  }
+}
+
+// Launches the persistent evaluator of every variant that can hold programs of stack need
+// <= max_stack, each over its own bucket (lists / counts written by the bucket kernel).
+static gp_status launch_variants(gp_context* ctx, EvalArgs a, const EvalPlan& pl, int32_t max_stack,
+                                 bool predict) {
+  const int32_t n = a.n_programs;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (ctx->profiling && !predict) {
+    if (!ctx->ev_free.empty()) { ev = ctx->ev_free.back(); ctx->ev_free.pop_back(); }
+    else { cudaEventCreate(&ev.first); cudaEventCreate(&ev.second); }
+    cudaEventRecord(ev.first, ctx->stream);
+  }
+  for (int v = 0; v < kNumVariants; ++v) {
+    if (v > 0 && kVariantStack[v - 1] >= max_stack) break;
+    const EvalVariant& var = variant(v);
+    a.stream = (const uint4*)ctx->codestream.p;
+    a.gstart = (const int64_t*)ctx->gstart.p + (int64_t)v * (n + 1);
+    a.prog_ids = (const int32_t*)ctx->lists.p + (int64_t)v * n;
+    a.prog_count = (const int32_t*)ctx->counts.p + v;
+    a.work_counter = (int32_t*)ctx->counts.p + kNumVariants + v;
+    const int occ = std::max(1, var.occupancy(predict, pl.xsmem, pl.smem));
+    gp_status s = ctx->cuda(var.launch(a, predict, pl.xsmem, ctx->sms * occ, pl.smem, ctx->stream),
+                            predict ? "predict kernel" : "eval kernel");
+    if (s) return s;
+  }
+  if (ctx->profiling && !predict) {
+    cudaEventRecord(ev.second, ctx->stream);
+    ctx->ev_pending.push_back(ev);
+  }
+  return GP_OK;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -271,11 +298,12 @@ gp_status gp_context_set_reference_row(gp_context* ctx, const float* x_ref, int3
   return ctx->cuda(cudaStreamSynchronize(ctx->stream), "xref sync");
 }
 
-// Shared front half of gp_evaluate / gp_predict: argument checks, staging, compile.
+// Shared front half of gp_evaluate / gp_predict: argument checks, staging, compile (stage),
+// Pearson shift, bucketing by stack need and the per-variant code streams (pack).
 static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_t*& offsets,
                          int32_t n_programs, int64_t n_nodes, int32_t max_stack, const float*& X,
-                         int64_t ldx, int64_t n_rows, int32_t n_cols, bool* any_host,
-                         const EvalVariant** var) {
+                         int64_t ldx, int64_t n_rows, int32_t n_cols, int32_t G, bool pearson,
+                         const float* y, bool* any_host) {
   if (n_programs < 1 || n_nodes < 1 || max_stack < 1 || max_stack > GP_MAX_STACK || n_rows < 1 ||
       n_cols < 1 || ldx < n_rows || !programs || !offsets || !X)
     return ctx->fail(GP_ERR_ARG, "invalid argument (n_programs=%d n_nodes=%lld max_stack=%d "
@@ -290,16 +318,54 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   const size_t xbytes = ((size_t)(n_cols - 1) * ldx + n_rows) * sizeof(float);
   if ((s = ctx->stage_in(X, xbytes, ctx->h_X, &d, any_host))) return s;
   X = (const float*)d;
-  const EvalVariant& v = pick_variant(max_stack);
-  *var = &v;
-  if ((s = ctx->grow(&ctx->code.p, &ctx->code.cap, (size_t)(n_nodes + 2) * sizeof(uint2), "code"))) return s;
-  if ((s = ctx->grow(&ctx->code_off.p, &ctx->code_off.cap, (size_t)n_programs * sizeof(int64_t), "code_off"))) return s;
-  if ((s = ctx->grow(&ctx->code_len.p, &ctx->code_len.cap, (size_t)n_programs * sizeof(int32_t), "code_len"))) return s;
-  if ((s = ctx->grow(&ctx->status.p, &ctx->status.cap, (size_t)n_programs * sizeof(uint32_t), "status"))) return s;
-  return ctx->cuda(launch_stage(programs, offsets, n_programs, n_nodes, n_cols, v.shape.stack,
-                                (uint2*)ctx->code.p, (int64_t*)ctx->code_off.p,
-                                (int32_t*)ctx->code_len.p, (uint32_t*)ctx->status.p, ctx->stream),
-                   "stage kernel");
+  const int64_t n = n_programs;
+  if ((s = ctx->grow(&ctx->code.p, &ctx->code.cap, (size_t)(n_nodes + 2) * sizeof(uint4), "code"))) return s;
+  if ((s = ctx->grow(&ctx->code_off.p, &ctx->code_off.cap, (size_t)n * sizeof(int64_t), "code_off"))) return s;
+  if ((s = ctx->grow(&ctx->code_len.p, &ctx->code_len.cap, (size_t)n * sizeof(int32_t), "code_len"))) return s;
+  if ((s = ctx->grow(&ctx->need.p, &ctx->need.cap, (size_t)n * sizeof(int32_t), "need"))) return s;
+  if ((s = ctx->grow(&ctx->lists.p, &ctx->lists.cap, (size_t)n * kNumVariants * sizeof(int32_t), "lists"))) return s;
+  if ((s = ctx->grow(&ctx->pos.p, &ctx->pos.cap, (size_t)n * kNumVariants * sizeof(int64_t), "pos"))) return s;
+  if ((s = ctx->grow(&ctx->gstart.p, &ctx->gstart.cap, (size_t)(n + 1) * kNumVariants * sizeof(int64_t), "gstart"))) return s;
+  if ((s = ctx->grow(&ctx->counts.p, &ctx->counts.cap, 2 * kNumVariants * sizeof(int32_t) + (kNumVariants + 1) * sizeof(int64_t), "counts"))) return s;
+  // stream words <= SUB_max x (code words + one marker per program) + 2 pad words
+  if ((s = ctx->grow(&ctx->codestream.p, &ctx->codestream.cap, ((size_t)4 * (n_nodes + n) + 2) * sizeof(uint4), "stream"))) return s;
+  if ((s = ctx->grow(&ctx->status.p, &ctx->status.cap, (size_t)n * sizeof(uint32_t), "status"))) return s;
+  if ((s = ctx->cuda(launch_stage(programs, offsets, n_programs, n_nodes, n_cols, max_stack,
+                                  (uint4*)ctx->code.p, (int64_t*)ctx->code_off.p,
+                                  (int32_t*)ctx->code_len.p, (int32_t*)ctx->need.p,
+                                  (uint32_t*)ctx->status.p, ctx->stream), "stage kernel"))) return s;
+  const float* shift = nullptr;
+  if (pearson) {  // DESIGN.md C9: K_p = f_p(reference row), K_y = y_ref
+    if ((s = ctx->grow(&ctx->shift.p, &ctx->shift.cap, (size_t)n * sizeof(float) + 16, "shift"))) return s;
+    float* sh = (float*)ctx->shift.p;
+    const float *xref, *yref;
+    int64_t stride;
+    if (ctx->xref_cols >= n_cols) {
+      xref = (const float*)ctx->xref.p;
+      stride = 1;
+      yref = (const float*)ctx->xref.p + ctx->xref_cols;
+    } else {
+      xref = X;
+      stride = ldx;
+      yref = y;
+    }
+    if ((s = ctx->cuda(launch_copy_scalar(yref, sh + n, ctx->stream), "y shift"))) return s;
+    if ((s = ctx->cuda(launch_shift((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
+                                    (const int32_t*)ctx->code_len.p, n_programs, kCaseStride,
+                                    xref, stride, sh, ctx->stream), "shift kernel"))) return s;
+    shift = sh;
+  }
+  int32_t* counts = (int32_t*)ctx->counts.p;
+  int64_t* base = (int64_t*)(counts + 2 * kNumVariants);
+  if ((s = ctx->cuda(launch_bucket((const int32_t*)ctx->need.p, (const int32_t*)ctx->code_len.p,
+                                   n_programs, G, (int32_t*)ctx->lists.p, (int64_t*)ctx->pos.p,
+                                   (int64_t*)ctx->gstart.p, counts, base, ctx->stream),
+                     "bucket kernel"))) return s;
+  return ctx->cuda(launch_pack((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
+                               (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->lists.p,
+                               (const int64_t*)ctx->pos.p, counts, base, shift, n_programs, G,
+                               (uint4*)ctx->codestream.p, ctx->stream),
+                   "pack kernel");
 }
 
 gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
@@ -313,10 +379,7 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
   if ((int)metric < 0 || (int)metric > GP_PEARSON || !y || !fitness_out)
     return ctx->fail(GP_ERR_ARG, "invalid metric / y / fitness_out");
   bool any_host = false;
-  const EvalVariant* v = nullptr;
-  gp_status s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx,
-                        n_rows, n_cols, &any_host, &v);
-  if (s) return s;
+  gp_status s;
   const void* d;
   if ((s = ctx->stage_in(y, (size_t)n_rows * sizeof(float), ctx->h_y, &d, &any_host))) return s;
   y = (const float*)d;
@@ -327,39 +390,15 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
   const bool fit_host = is_host_pointer(fitness_out);
   const bool st_host = status_out && is_host_pointer(status_out);
   const int S = metric == GP_PEARSON ? 3 : 1;
-
-  // Pearson reference row and shift (C9)
-  if (metric == GP_PEARSON) {
-    if ((s = ctx->grow(&ctx->shift.p, &ctx->shift.cap, (size_t)n_programs * sizeof(float) + 16, "shift"))) return s;
-    float* shift = (float*)ctx->shift.p;
-    const float* xref;
-    int64_t stride;
-    const float* yref;
-    if (ctx->xref_cols >= n_cols) {
-      xref = (const float*)ctx->xref.p;
-      stride = 1;
-      yref = (const float*)ctx->xref.p + ctx->xref_cols;
-    } else {
-      xref = X;
-      stride = ldx;
-      yref = y;
-    }
-    float* yshift = shift + n_programs;
-    if ((s = ctx->cuda(launch_copy_scalar(yref, yshift, ctx->stream), "y shift"))) return s;
-    if ((s = ctx->cuda(launch_shift((const uint2*)ctx->code.p, (const int64_t*)ctx->code_off.p,
-                                    (const int32_t*)ctx->code_len.p, n_programs, v->shape.stack,
-                                    xref, stride, shift, ctx->stream), "shift kernel"))) return s;
-  }
+  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, S, false);
+  if ((s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, n_rows,
+                   n_cols, pl.G, metric == GP_PEARSON, y, &any_host))) return s;
 
   // Fused evaluation -> partial sums
-  EvalPlan pl = plan_eval(*v, ctx->device, n_rows, n_programs, n_cols, S, false);
   const int64_t ld_part = (int64_t)n_programs * S + 3;
   if ((s = ctx->grow(&ctx->partial.p, &ctx->partial.cap, (size_t)pl.n_chunks * ld_part * sizeof(double), "partial"))) return s;
   if ((s = ctx->grow(&ctx->sums.p, &ctx->sums.cap, (size_t)ld_part * sizeof(double), "sums"))) return s;
   EvalArgs a{};
-  a.code = (const uint2*)ctx->code.p;
-  a.code_off = (const int64_t*)ctx->code_off.p;
-  a.code_len = (const int32_t*)ctx->code_len.p;
   a.X = X;
   a.ldx = ldx;
   a.y = y;
@@ -370,23 +409,15 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
   a.metric = metric;
   a.G = pl.G;
   a.rows_per_chunk = pl.rows_per_chunk;
+  a.n_chunks = pl.n_chunks;
   a.partial = (double*)ctx->partial.p;
   a.ld_part = ld_part;
-  a.shift = metric == GP_PEARSON ? (const float*)ctx->shift.p : nullptr;
   a.y_shift = metric == GP_PEARSON ? (const float*)ctx->shift.p + n_programs : nullptr;
   ctx->last_plan = pl;
-  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-  if (ctx->profiling) {
-    if (!ctx->ev_free.empty()) { ev = ctx->ev_free.back(); ctx->ev_free.pop_back(); }
-    else { cudaEventCreate(&ev.first); cudaEventCreate(&ev.second); }
-    cudaEventRecord(ev.first, ctx->stream);
-  }
-  if ((s = ctx->cuda(v->launch(a, false, pl.xsmem, dim3((unsigned)pl.n_chunks, (unsigned)pl.n_groups),
-                               pl.smem, ctx->stream), "eval kernel"))) return s;
-  if (ctx->profiling) {
-    cudaEventRecord(ev.second, ctx->stream);
-    ctx->ev_pending.push_back(ev);
-  }
+  if ((s = ctx->cuda(launch_consts(y, w, n_rows, pl.rows_per_chunk, pl.n_chunks, a.y_shift,
+                                   a.partial, ld_part, (int64_t)n_programs * S, ctx->stream),
+                     "consts kernel"))) return s;
+  if ((s = launch_variants(ctx, a, pl, max_stack, false))) return s;
   if ((s = ctx->cuda(launch_tile_reduce((const double*)ctx->partial.p, pl.n_chunks, ld_part,
                                         (double*)ctx->sums.p, ctx->stream), "tile_reduce"))) return s;
   // A6: one all-reduce of the fp64 partial sums across ranks (rows are sharded)
@@ -426,15 +457,11 @@ gp_status gp_predict(gp_context* ctx, const gp_node* programs, const int64_t* no
   cudaSetDevice(ctx->device);
   if (!out || ld_out < n_rows) return ctx->fail(GP_ERR_ARG, "invalid out / ld_out");
   bool any_host = false;
-  const EvalVariant* v = nullptr;
+  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, 1, true);
   gp_status s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx,
-                        n_rows, n_cols, &any_host, &v);
+                        n_rows, n_cols, pl.G, false, nullptr, &any_host);
   if (s) return s;
-  EvalPlan pl = plan_eval(*v, ctx->device, n_rows, n_programs, n_cols, 1, true);
   EvalArgs a{};
-  a.code = (const uint2*)ctx->code.p;
-  a.code_off = (const int64_t*)ctx->code_off.p;
-  a.code_len = (const int32_t*)ctx->code_len.p;
   a.X = X;
   a.ldx = ldx;
   a.n_rows = n_rows;
@@ -443,10 +470,10 @@ gp_status gp_predict(gp_context* ctx, const gp_node* programs, const int64_t* no
   a.metric = GP_MSE;
   a.G = pl.G;
   a.rows_per_chunk = pl.rows_per_chunk;
+  a.n_chunks = pl.n_chunks;
   a.out = out;
   a.ld_out = ld_out;
-  if ((s = ctx->cuda(v->launch(a, true, pl.xsmem, dim3((unsigned)pl.n_chunks, (unsigned)pl.n_groups),
-                               pl.smem, ctx->stream), "predict kernel"))) return s;
+  if ((s = launch_variants(ctx, a, pl, max_stack, true))) return s;
   if (status_out) {
     const bool st_host = is_host_pointer(status_out);
     if ((s = ctx->cuda(cudaMemcpyAsync(status_out, ctx->status.p, (size_t)n_programs * sizeof(uint32_t),

@@ -11,18 +11,28 @@
 namespace gpb {
 
 // ---------------------------------------------------------------------------------------------
-// Stage / compile. One thread per program (programs are short; this is a few µs).
+// Stage / compile. One thread per program (programs are short; a few µs total).
 //  - prefix validation with the needed-counter scan, opcode and variable-range checks
-//  - reverse (evaluation-order) emission with the static stack slot of every node
-//  - stack need = max occupancy; > capacity -> GP_FLAG_STACK_OVERFLOW
+//  - reverse (evaluation-order) walk that folds every terminal into its parent's code word
+//    and assigns the static destination slot of every emitted node (device_ops.cuh "compiled
+//    program code"); stack need = max occupancy; > capacity -> GP_FLAG_STACK_OVERFLOW
 // Invalid programs get code_len = 0 and are skipped by every later kernel.
 // ---------------------------------------------------------------------------------------------
+namespace {
+struct Operand {        // pending operand during the reverse walk
+  uint32_t kind;        // 0 stack value, 1 variable, 2 constant
+  uint32_t payload;     // variable index or fp32 bits
+};
+constexpr int kMaxPending = 64;
+}  // namespace
+
 __global__ void stage_kernel(const gp_node* __restrict__ nodes, const int64_t* __restrict__ off,
                              int32_t n_programs, int64_t n_nodes, int32_t n_cols, int32_t cap,
-                             uint2* __restrict__ code, int64_t* __restrict__ code_off,
-                             int32_t* __restrict__ code_len, uint32_t* __restrict__ status) {
+                             uint4* __restrict__ code, int64_t* __restrict__ code_off,
+                             int32_t* __restrict__ code_len, int32_t* __restrict__ need_out,
+                             uint32_t* __restrict__ status) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p == 0) code[n_nodes] = code[n_nodes + 1] = make_uint2(0u, 0u);  // prefetch pad words
+  if (p == 0) code[n_nodes] = code[n_nodes + 1] = make_uint4(0u, 0u, 0u, 0u);  // prefetch pads
   if (p >= n_programs) return;
   const int64_t b = off[p], e = off[p + 1];
   uint32_t flags = 0;
@@ -34,39 +44,257 @@ __global__ void stage_kernel(const gp_node* __restrict__ nodes, const int64_t* _
       if (needed == 0) { flags |= GP_FLAG_INVALID_PREFIX; break; }
       const gp_node nd = nodes[i];
       const int a = op_arity(nd.op);
-      if (a < 0 || nd.op < 0) { flags |= GP_FLAG_BAD_OPCODE; break; }
+      if (a < 0) { flags |= GP_FLAG_BAD_OPCODE; break; }
       if (nd.op == GP_OP_VAR && (nd.var < 0 || nd.var >= n_cols)) flags |= GP_FLAG_VAR_RANGE;
       needed += a - 1;
     }
     if (!(flags & GP_FLAG_BAD_OPCODE) && needed != 0) flags |= GP_FLAG_INVALID_PREFIX;
   }
+  int64_t emitted = 0;
+  int need = 0;
   if (!flags) {
-    const int64_t len = e - b;
-    int sp = 0, need = 0;
-    for (int64_t k = 0; k < len; ++k) {
-      const gp_node nd = nodes[e - 1 - k];
+    Operand pend[kMaxPending];
+    int np = 0, sp = 0;
+    auto emit = [&](int opv, int slot, uint32_t pa, uint32_t pb) {
+      code[b + emitted++] = make_uint4((uint32_t)(opv * kCaseStride + slot) * 4u, pa, pb, 0u);
+    };
+    for (int64_t i = e - 1; i >= b && !flags; --i) {
+      const gp_node nd = nodes[i];
       const int a = op_arity(nd.op);
-      const int slot = a == 0 ? sp : sp - a;  // terminal pushes at sp; f writes over its operands
-      sp += 1 - a;
+      if (a == 0) {
+        if (np == kMaxPending) { flags |= GP_FLAG_STACK_OVERFLOW; break; }
+        pend[np++] = Operand{nd.op == GP_OP_VAR ? 1u : 2u, nd.op == GP_OP_VAR ? (uint32_t)nd.var
+                                                                              : __float_as_uint(nd.value)};
+        continue;
+      }
+      if (a == 1) {
+        const Operand A = pend[--np];
+        int slot;
+        if (A.kind == 0) { slot = sp - 1; emit(opv_un(nd.op, UV_S), slot, 0u, 0u); }
+        else { slot = sp; emit(opv_un(nd.op, A.kind == 1 ? UV_V : UV_C), slot, A.payload, 0u); }
+        sp = slot + 1;
+      } else {
+        const Operand A = pend[--np];   // first pop = first operand
+        const Operand B = pend[--np];
+        int v, slot;
+        if (A.kind == 0 && B.kind == 0) { v = BV_SS; slot = sp - 2; }
+        else if (A.kind == 0) { v = B.kind == 1 ? BV_SV : BV_SC; slot = sp - 1; }
+        else if (B.kind == 0) { v = A.kind == 1 ? BV_VS : BV_CS; slot = sp - 1; }
+        else {
+          v = A.kind == 1 ? (B.kind == 1 ? BV_VV : BV_VC) : (B.kind == 1 ? BV_CV : BV_CC);
+          slot = sp;
+        }
+        emit(opv_bin(nd.op, v), slot, A.payload, B.payload);
+        sp = slot + 1;
+      }
+      pend[np++] = Operand{0u, 0u};
       need = need > sp ? need : sp;
-      if (need > cap) break;
-      const uint32_t payload = nd.op == GP_OP_VAR ? ((uint32_t)nd.var << kCaseBits) : 0u;
-      code[b + k] = make_uint2((uint32_t)(nd.op * cap + slot) | payload, __float_as_uint(nd.value));
+      if (need > cap) flags |= GP_FLAG_STACK_OVERFLOW;
     }
-    if (need > cap) flags |= GP_FLAG_STACK_OVERFLOW;
+    if (!flags && pend[0].kind != 0) {  // lone terminal program: one push
+      emit(pend[0].kind == 1 ? OPV_PUSH_V : OPV_PUSH_C, 0, pend[0].payload, 0u);
+      need = 1;
+    }
   }
+  need_out[p] = need;
   code_off[p] = b;
-  code_len[p] = flags ? 0 : (int32_t)(e - b);
+  code_len[p] = flags ? 0 : (int32_t)emitted;
   status[p] = flags;
 }
 
 cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n_programs,
-                         int64_t n_nodes, int32_t n_cols, int32_t stack_cap, uint2* code,
-                         int64_t* code_off, int32_t* code_len, uint32_t* status, cudaStream_t s) {
+                         int64_t n_nodes, int32_t n_cols, int32_t max_stack, uint4* code,
+                         int64_t* code_off, int32_t* code_len, int32_t* need, uint32_t* status,
+                         cudaStream_t s) {
   const int nt = 128;
   stage_kernel<<<(n_programs + nt - 1) / nt, nt, 0, s>>>(nodes, offsets, n_programs, n_nodes,
-                                                          n_cols, stack_cap, code, code_off,
-                                                          code_len, status);
+                                                          n_cols, max_stack, code, code_off,
+                                                          code_len, need, status);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Bucketing by stack need + code-stream layout (one CTA of 1024 threads). Program p goes to the
+// first variant whose register stack holds its need; each bucket list keeps ascending program
+// order (deterministic). Each variant's stream holds, per program, SUB_b x (code words + 1 marker);
+// pos / gstart are absolute stream offsets (group g of bucket b starts at gstart[b][g]).
+// ---------------------------------------------------------------------------------------------
+namespace {
+// Block-wide exclusive scan of one int64 per thread (1024 threads); returns the block total.
+__device__ int64_t block_exclusive_scan(int64_t v, int64_t* out, int64_t* warp_tot) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int64_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t t = warp_tot[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_tot[lane] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  *out = (warp ? warp_tot[warp - 1] : 0) + x - v;
+  const int64_t total = warp_tot[31];
+  __syncthreads();
+  return total;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict__ need,
+                                                      const int32_t* __restrict__ code_len,
+                                                      int32_t n, int32_t G,
+                                                      int32_t* __restrict__ lists,
+                                                      int64_t* __restrict__ pos,
+                                                      int64_t* __restrict__ gstart,
+                                                      int32_t* __restrict__ counts,
+                                                      int64_t* __restrict__ base) {
+  __shared__ int warp_cnt[kNumVariants][32];
+  __shared__ int cnt[kNumVariants];
+  __shared__ int64_t warp_tot[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int caps[kNumVariants] = {4, 8, 12, 20};   // kVariantStack
+  const int subs[kNumVariants] = {1, 2, 4, 4};     // kVariantSub
+  if (tid < kNumVariants) { cnt[tid] = 0; counts[kNumVariants + tid] = 0; }  // work counters
+  __syncthreads();
+  // phase 1: stable partition by stack need
+  for (int c0 = 0; c0 < n; c0 += 1024) {
+    const int p = c0 + tid;
+    int b = -1;
+    if (p < n && code_len[p] > 0) {
+      b = kNumVariants - 1;
+      for (int v = kNumVariants - 1; v >= 0; --v)
+        if (need[p] <= caps[v]) b = v;
+    }
+    int rank[kNumVariants];
+    for (int v = 0; v < kNumVariants; ++v) {
+      const unsigned m = __ballot_sync(0xffffffffu, b == v);
+      rank[v] = __popc(m & ((1u << lane) - 1u));
+      if (lane == 0) warp_cnt[v][warp] = __popc(m);
+    }
+    __syncthreads();
+    if (b >= 0) {
+      int off = cnt[b] + rank[b];
+      for (int w2 = 0; w2 < warp; ++w2) off += warp_cnt[b][w2];
+      lists[(int64_t)b * n + off] = p;
+    }
+    __syncthreads();
+    if (tid < kNumVariants) {
+      int t = 0;
+      for (int w2 = 0; w2 < 32; ++w2) t += warp_cnt[tid][w2];
+      cnt[tid] += t;
+    }
+    __syncthreads();
+  }
+  // phase 2: stream offsets per bucket (words = SUB x (len + 1) per program)
+  int64_t running = 0;
+  for (int b = 0; b < kNumVariants; ++b) {
+    const int cb = cnt[b];
+    if (tid == 0) base[b] = running;
+    for (int c0 = 0; c0 < cb; c0 += 1024) {
+      const int j = c0 + tid;
+      const int64_t words = j < cb ? (int64_t)subs[b] * (code_len[lists[(int64_t)b * n + j]] + 1) : 0;
+      int64_t ex;
+      const int64_t tot = block_exclusive_scan(words, &ex, warp_tot);
+      if (j < cb) {
+        pos[(int64_t)b * n + j] = running + ex;
+        if (j % G == 0) gstart[(int64_t)b * (n + 1) + j / G] = running + ex;
+      }
+      running += tot;
+    }
+    if (tid == 0) gstart[(int64_t)b * (n + 1) + (cb + G - 1) / G] = running;
+    __syncthreads();
+  }
+  if (tid == 0) base[kNumVariants] = running;
+  if (tid < kNumVariants) counts[tid] = cnt[tid];
+}
+
+cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
+                          int32_t G, int32_t* lists, int64_t* pos, int64_t* gstart,
+                          int32_t* counts, int64_t* base, cudaStream_t s) {
+  bucket_kernel<<<1, 1024, 0, s>>>(need, code_len, n_programs, G, lists, pos, gstart, counts,
+                                   base);
+  return cudaGetLastError();
+}
+
+// One thread per (bucket, list entry): SUB copies of the program's code, each followed by a
+// marker word: END_PASS {case, p, next pass, K_p bits} or END {case, p, index in group, K_p bits}.
+__global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __restrict__ code_off,
+                            const int32_t* __restrict__ code_len, const int32_t* __restrict__ lists,
+                            const int64_t* __restrict__ pos, const int32_t* __restrict__ counts,
+                            const int64_t* __restrict__ base, const float* __restrict__ shift,
+                            int32_t n, int32_t G, uint4* __restrict__ stream) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) stream[base[kNumVariants]] = stream[base[kNumVariants] + 1] = make_uint4(0, 0, 0, 0);
+  if (i >= (int64_t)kNumVariants * n) return;
+  const int b = (int)(i / n), j = (int)(i % n);
+  if (j >= counts[b]) return;
+  const int subs[kNumVariants] = {1, 2, 4, 4};
+  const int p = lists[i];
+  const int len = code_len[p];
+  const uint4* src = code + code_off[p];
+  const uint32_t kp = shift ? __float_as_uint(shift[p]) : 0u;
+  uint4* dst = stream + pos[i];
+  for (int pass = 0; pass < subs[b]; ++pass) {
+    for (int k = 0; k < len; ++k) *dst++ = src[k];
+    const bool last = pass == subs[b] - 1;
+    *dst++ = last ? make_uint4((uint32_t)kCaseEnd * 4u, (uint32_t)p, (uint32_t)(j % G), kp)
+                  : make_uint4((uint32_t)kCaseEndPass * 4u, (uint32_t)p, (uint32_t)(pass + 1), kp);
+  }
+}
+
+cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
+                        const int32_t* lists, const int64_t* pos, const int32_t* counts,
+                        const int64_t* base, const float* shift, int32_t n_programs, int32_t G,
+                        uint4* stream, cudaStream_t s) {
+  const int nt = 256;
+  const int64_t total = (int64_t)kNumVariants * n_programs;
+  pack_kernel<<<(unsigned)((total + nt - 1) / nt), nt, 0, s>>>(code, code_off, code_len, lists,
+                                                               pos, counts, base, shift,
+                                                               n_programs, G, stream);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Dataset constants per row chunk (program independent): W = sum w, S_y = sum w (y - K_y),
+// S_yy = sum w (y - K_y)^2 over live rows (w != 0), fp64, fixed order.
+// ---------------------------------------------------------------------------------------------
+__global__ void consts_kernel(const float* __restrict__ y, const float* __restrict__ w,
+                              int64_t n_rows, int64_t rows_per_chunk, const float* y_shift,
+                              double* __restrict__ partial, int64_t ld_part, int64_t col0) {
+  __shared__ double red[3][256];
+  const int q = blockIdx.x, tid = threadIdx.x;
+  const int64_t r0 = (int64_t)q * rows_per_chunk, r1 = min(r0 + rows_per_chunk, n_rows);
+  const float Ky = y_shift ? *y_shift : 0.0f;
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+  for (int64_t i = r0 + tid; i < r1; i += 256) {
+    const double wi = w ? (double)w[i] : 1.0;
+    if (wi != 0.0) {
+      const double yc = (double)(y[i] - Ky);
+      c0 += wi;
+      c1 += wi * yc;
+      c2 += wi * yc * yc;
+    }
+  }
+  red[0][tid] = c0; red[1][tid] = c1; red[2][tid] = c2;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) for (int k = 0; k < 3; ++k) red[k][tid] += red[k][tid + o];
+    __syncthreads();
+  }
+  if (tid < 3) partial[(int64_t)q * ld_part + col0 + tid] = red[tid][0];
+}
+
+cudaError_t launch_consts(const float* y, const float* w, int64_t n_rows, int64_t rows_per_chunk,
+                          int64_t n_chunks, const float* y_shift, double* partial, int64_t ld_part,
+                          int64_t col0, cudaStream_t s) {
+  consts_kernel<<<(unsigned)n_chunks, 256, 0, s>>>(y, w, n_rows, rows_per_chunk, y_shift, partial,
+                                                    ld_part, col0);
   return cudaGetLastError();
 }
 
@@ -74,8 +302,8 @@ cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n
 // Pearson shift (C9): K_p = f_p(x_ref), evaluated with the SAME fp32 op code as the
 // register-stack evaluator so a constant program gives d = yhat - K_p = 0 exactly on every row.
 // ---------------------------------------------------------------------------------------------
-__global__ void shift_kernel(const uint2* __restrict__ code, const int64_t* __restrict__ code_off,
-                             const int32_t* __restrict__ code_len, int32_t n_programs, int32_t cap,
+__global__ void shift_kernel(const uint4* __restrict__ code, const int64_t* __restrict__ code_off,
+                             const int32_t* __restrict__ code_len, int32_t n_programs,
                              const float* __restrict__ xref, int64_t stride,
                              float* __restrict__ shift) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -83,24 +311,43 @@ __global__ void shift_kernel(const uint2* __restrict__ code, const int64_t* __re
   const int len = code_len[p];
   if (len == 0) { shift[p] = 0.0f; return; }
   float stk[GP_MAX_STACK + 1];
-  const uint2* pc = code + code_off[p];
+  const uint4* pc = code + code_off[p];
+  auto term = [&](int src, uint32_t pl) {   // 1 variable, 2 constant
+    return src == 1 ? xref[(int64_t)pl * stride] : __uint_as_float(pl);
+  };
   for (int k = 0; k < len; ++k) {
-    const uint2 cw = pc[k];
-    const int id = (int)(cw.x & kCaseMask), kind = id / cap, slot = id - kind * cap;
-    if (kind == GP_OP_VAR) stk[slot] = xref[(int64_t)(cw.x >> kCaseBits) * stride];
-    else if (kind == GP_OP_CONST) stk[slot] = __uint_as_float(cw.y);
-    else if (op_arity(kind) == 1) stk[slot] = apply_rt(kind, stk[slot], 0.0f);
-    else stk[slot] = apply_rt(kind, stk[slot + 1], stk[slot]);
+    const uint4 cw = pc[k];
+    const int id = (int)(cw.x >> 2), opv = id / kCaseStride, slot = id - opv * kCaseStride;
+    if (opv < OPV_BIN0) {
+      stk[slot] = term(opv == OPV_PUSH_V ? 1 : 2, cw.y);
+    } else if (opv < OPV_UN0) {
+      const int op = GP_OP_ADD + (opv - OPV_BIN0) / 9, v = (opv - OPV_BIN0) % 9;
+      float a, bb;
+      switch (v) {
+        case BV_SS: a = stk[slot + 1]; bb = stk[slot]; break;
+        case BV_SV: case BV_SC: a = stk[slot]; bb = term(v == BV_SV ? 1 : 2, cw.z); break;
+        case BV_VS: case BV_CS: a = term(v == BV_VS ? 1 : 2, cw.y); bb = stk[slot]; break;
+        default:
+          a = term(v == BV_VV || v == BV_VC ? 1 : 2, cw.y);
+          bb = term(v == BV_VV || v == BV_CV ? 1 : 2, cw.z);
+      }
+      stk[slot] = apply_rt(op, a, bb);
+    } else {
+      const int op = GP_OP_SIN + (opv - OPV_UN0) / 3, u = (opv - OPV_UN0) % 3;
+      const float a = u == UV_S ? stk[slot] : term(u == UV_V ? 1 : 2, cw.y);
+      stk[slot] = apply_rt(op, a, 0.0f);
+    }
   }
   shift[p] = stk[0];
 }
 
-cudaError_t launch_shift(const uint2* code, const int64_t* code_off, const int32_t* code_len,
+cudaError_t launch_shift(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                          int32_t n_programs, int32_t stack_cap, const float* xref,
                          int64_t xref_stride, float* shift_out, cudaStream_t s) {
   const int nt = 128;
+  (void)stack_cap;
   shift_kernel<<<(n_programs + nt - 1) / nt, nt, 0, s>>>(code, code_off, code_len, n_programs,
-                                                          stack_cap, xref, xref_stride, shift_out);
+                                                          xref, xref_stride, shift_out);
   return cudaGetLastError();
 }
 

@@ -165,14 +165,25 @@ __device__ __forceinline__ float apply_rt(int op, float a, float b) {
   return __int_as_float(0x7fc00000);
 }
 
-// ---- compiled program word (written by the stage kernel, read by the evaluator) ---------------
-// One uint2 per node, stored in EVALUATION order (reverse prefix):
-//   .x bits [0,10)  : case id = kind * STACK + slot, kind = op (0 var, 1 const, 2.. functions)
-//       bits [10,32): variable index (var nodes)
-//   .y              : fp32 constant bits (const nodes)
-// slot = destination stack slot, static per node (the occupancy before/after each node depends
-// only on the tree shape, never on data): terminal -> sp, unary -> sp-1, binary -> sp-2.
-constexpr int kCaseBits = 10;
-constexpr uint32_t kCaseMask = (1u << kCaseBits) - 1u;
+// ---- compiled program code (written by the stage kernel, read by the evaluator) ---------------
+// One uint4 per EMITTED node, in evaluation order (reverse prefix). Terminals are not
+// emitted on their own: each terminal operand is folded into its parent function's code word
+// ("superinstruction"), so only function nodes are dispatched (a lone-terminal program emits one
+// push). Word layout:
+//   .x = case id * 4 (byte offset into the dispatch jump table), case id = opv * STACK + slot
+//   .y = payload of the first operand a  (variable index, or fp32 constant bits)
+//   .z = payload of the second operand b (variable index, or fp32 constant bits)
+// opv enumerates (op, operand-source variant) pairs:
+//   0 push var, 1 push const;
+//   binary op o (2..8): 2 + (o-2)*9 + v, v = SS, SV, SC, VS, CS, VV, VC, CV, CC
+//       (S = stack, V = variable, C = constant; first letter = operand a, second = operand b)
+//   unary op o (9..25): 65 + (o-9)*3 + u, u = S, V, C
+// slot = destination stack slot (static: occupancy depends only on the tree shape):
+//   S,S -> a = st[slot+1], b = st[slot];  one S -> that operand is st[slot];  no S -> new slot.
+enum { OPV_PUSH_V = 0, OPV_PUSH_C = 1, OPV_BIN0 = 2, OPV_UN0 = 65, OPV_COUNT = 116 };
+enum { BV_SS = 0, BV_SV, BV_SC, BV_VS, BV_CS, BV_VV, BV_VC, BV_CV, BV_CC };
+enum { UV_S = 0, UV_V, UV_C };
+__host__ __device__ constexpr int opv_bin(int op, int v) { return OPV_BIN0 + (op - GP_OP_ADD) * 9 + v; }
+__host__ __device__ constexpr int opv_un(int op, int u) { return OPV_UN0 + (op - GP_OP_SIN) * 3 + u; }
 
 }  // namespace gpb

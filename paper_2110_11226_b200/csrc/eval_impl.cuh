@@ -1,29 +1,41 @@
 // eval_impl.cuh -- the fused population evaluator, sm_100a.
 //
-// Included by eval_s{8,12,20}.cu with GP_STACK (register-stack capacity), GP_R (rows per thread
-// per pass), GP_SUB (passes per program per tile) and GP_NT (threads per CTA) defined, so every
-// (op, slot) case of the dispatch switch is generated for exactly GP_STACK slots.
+// Included by eval_s{4,8,12,20}.cu with GP_STACK (register-stack capacity), GP_R (rows per thread
+// per pass), GP_SUB (passes per program per tile), GP_NT (threads per CTA) and GP_MINB (resident
+// CTAs per SM the register budget must allow) defined, so every (op, operand variant, slot) case of
+// the dispatch switch is generated for exactly GP_STACK slots.
 //
-// What one CTA does (work item = row chunk q x program group g; grid = (n_chunks, n_groups)):
-//   for each tile of TILE = NT*R*SUB rows of the chunk:
+// Persistent CTAs pull work items (program group g x row chunk q) from a queue. Per item:
+//   for each tile of TILE = NT*R*SUB = 2048 rows of the chunk:
 //     stage y, w (and X when n_cols is small) into shared memory, coalesced, zero-padded  [A2]
-//     for each program p of the group:                     -- warp-uniform: no divergence
-//       for each of SUB passes: run the compiled program on R rows per thread with the stack in
-//         REGISTERS: the stack slot of every node is static (stage kernel), so the dispatch is one
-//         switch on (op, slot) and no stack index is ever computed at run time  [A3]
+//     walk the group's packed code stream (aux.cu pack_kernel): for each program of the group
+//     (programs of this variant's stack-need bucket), SUB copies of its code, one per row pass,
+//     each closed by a marker word whose case does the loss / reduction -- one contiguous stream,
+//     so the 2-deep code prefetch never restarts at a program boundary:
+//       -- warp-uniform control flow: all lanes run the same program, no divergence
+//       for each of SUB passes: run the compiled code on R rows per thread with the stack in
+//         REGISTERS: the destination slot of every code word is static (stage kernel) and terminal
+//         operands are folded into their parent's word, so one jump-table branch per function
+//         node dispatches an (op, operand-source, slot) case; no stack index is ever computed at
+//         run time (the paper's unrolled slot loop, costs O(capacity) per push) [A3]
 //       fused weighted loss of those rows (no m x n prediction matrix)             [A4]
 //       warp shuffle reduction, lane 0 accumulates into a per-(warp, program) fp64 smem slot   [A5]
-//   per-(program) sums over warps in fixed order -> partial[q][p] (no atomics, deterministic)
+//   per-program sums over warps in fixed order -> partial[q][p] (no atomics on data: the sums do
+//   not depend on which CTA ran which item)
 //
 // The paper's design is one thread per row and a (ceil(m/256), n) grid; here each thread
-// owns R*SUB rows and loops over programs, so X is read from HBM once per program GROUP rather
-// than once per program, and node dispatch is amortised over R rows.
+// owns R*SUB rows and loops over programs, so X is read from HBM about once (program groups are
+// the fastest-varying work-item index, co-resident CTAs share row chunks through L2) and the
+// dispatch is amortised over R rows.
 #include <cfloat>
 #include "device_ops.cuh"
 #include "kernels.h"
 
 #ifndef GP_STACK
 #error "define GP_STACK"
+#endif
+#ifndef GP_MINB
+#define GP_MINB 1   // minimum resident CTAs per SM (register budget = 64K / (GP_MINB * NT))
 #endif
 
 #define GP_CAT2(a, b) a##b
@@ -36,70 +48,90 @@ namespace GP_NS {
 constexpr int STACK = GP_STACK, R = GP_R, SUB = GP_SUB, NT = GP_NT;
 constexpr int TILE = NT * R * SUB, NW = NT / 32, R4 = R / 4;
 static_assert(R % 4 == 0 && NT % 32 == 0, "R must be a multiple of 4");
-static_assert(GP_OP_COUNT * STACK <= (1 << kCaseBits), "case id must fit kCaseBits");
+static_assert(TILE == kTile, "every variant shares the row tile");
+static_assert(STACK <= kCaseStride, "slot must fit the case stride");
+
+// dynamic shared-memory opt-in: 227 KB per CTA minus the kernel's static shared memory
+constexpr int kMaxDynSmem = 220 * 1024;
 
 constexpr float kLogLossLo = 1.0000000000000005e-15f;  // -ln(1 - 1e-15), S:191 clamp (C7)
 constexpr float kLogLossHi = 34.538776394910684f;      // -ln(1e-15)
 
-// Shared-memory layout (bytes); G programs per group, S accumulators per program.
+// Shared-memory layout (bytes): fp64 accumulators [NW][G][S] | ys[TILE] | ws[TILE] | xs[n_cols][TILE]
 __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
-  return (((size_t)NW * G * S + NW * 3) * sizeof(double) + 15) & ~(size_t)15;
-}
-__host__ __device__ inline size_t smem_bytes(int G, int S, int n_cols, bool xsmem) {
-  return smem_acc_bytes(G, S) + 2 * TILE * sizeof(float) +
-         (xsmem ? (size_t)n_cols * TILE * sizeof(float) : 0);
+  return ((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15;
 }
 
-#define LBL(OP, s) ((OP) * STACK + (s))
+#define LBL(OPV, s) ((OPV) * kCaseStride + (s))
 
 // -- dispatch cases -------------------------------------------------------------------------------
-// Variable push: from shared memory (xsmem: LDS.128 per 4 rows) or from global memory via L1.
-#define GP_LOAD_VAR(s)                                                                         \
-  {                                                                                            \
-    const int var = (int)(cw.x >> kCaseBits);                                                  \
-    if constexpr (XSMEM) {                                                                     \
-      const float4* xv = reinterpret_cast<const float4*>(xs + var * TILE + ebase);             \
-      _Pragma("unroll") for (int k = 0; k < R4; ++k) {                                         \
-        const float4 v = xv[k * NT];                                                           \
-        st[s][4 * k] = v.x; st[s][4 * k + 1] = v.y; st[s][4 * k + 2] = v.z;                    \
-        st[s][4 * k + 3] = v.w;                                                                \
-      }                                                                                        \
-    } else {                                                                                   \
-      const float* xv = a.X + (int64_t)var * a.ldx + t0;                                       \
-      _Pragma("unroll") for (int r = 0; r < R; ++r) {                                          \
-        const int e = min(ebase + (r >> 2) * NT * 4 + (r & 3), nvalid - 1);                    \
-        st[s][r] = __ldg(xv + e);                                                              \
-      }                                                                                        \
+// Operand fetch of a variable into R registers: from the shared-memory tile (LDS.128 per 4 rows)
+// or, for wide datasets, from global memory through L1/L2 (rows clamped into the tile).
+#define GP_FETCH_VAR(t, var)                                                                   \
+  if constexpr (XSMEM) {                                                                       \
+    const float4* xv = reinterpret_cast<const float4*>(xs + (int)(var) * TILE + ebase);        \
+    _Pragma("unroll") for (int k = 0; k < R4; ++k) {                                           \
+      const float4 v = xv[k * NT];                                                             \
+      t[4 * k] = v.x; t[4 * k + 1] = v.y; t[4 * k + 2] = v.z; t[4 * k + 3] = v.w;              \
     }                                                                                          \
+  } else {                                                                                     \
+    const float* xv = a.X + (int64_t)(var) * a.ldx + t0;                                       \
+    _Pragma("unroll") for (int r = 0; r < R; ++r)                                              \
+      t[r] = __ldg(xv + min(ebase + (r >> 2) * NT * 4 + (r & 3), nvalid - 1));                 \
   }
-#define GP_TERM(s)                                                                             \
-  case LBL(GP_OP_VAR, s): GP_LOAD_VAR(s) break;                                                \
-  case LBL(GP_OP_CONST, s): {                                                                  \
-    const float c = __uint_as_float(cw.y);                                                     \
-    _Pragma("unroll") for (int r = 0; r < R; ++r) st[s][r] = c;                                \
-  } break;
-#define GP_UN(OP, s)                                                                           \
-  case LBL(OP, s): {                                                                           \
-    _Pragma("unroll") for (int r = 0; r < R; ++r) st[s][r] = apply1<OP>(st[s][r]);             \
-  } break;
-#define GP_BIN(OP, s)                                                                          \
-  case LBL(OP, s): {                                                                           \
-    _Pragma("unroll") for (int r = 0; r < R; ++r) st[s][r] = apply2<OP>(st[(s) + 1][r], st[s][r]); \
-  } break;
-#define GP_SLOT_TU(s)                                                                          \
-  GP_TERM(s) GP_UN(GP_OP_SIN, s) GP_UN(GP_OP_COS, s) GP_UN(GP_OP_TAN, s) GP_UN(GP_OP_ABS, s)   \
-  GP_UN(GP_OP_NEG, s) GP_UN(GP_OP_SQRT, s) GP_UN(GP_OP_LOG, s) GP_UN(GP_OP_EXP, s)             \
-  GP_UN(GP_OP_INV, s) GP_UN(GP_OP_SQUARE, s) GP_UN(GP_OP_CUBE, s) GP_UN(GP_OP_TANH, s)         \
-  GP_UN(GP_OP_SINH, s) GP_UN(GP_OP_COSH, s) GP_UN(GP_OP_ASIN, s) GP_UN(GP_OP_ACOS, s)          \
-  GP_UN(GP_OP_ATAN, s)
-#define GP_SLOT_B(s)                                                                           \
-  GP_BIN(GP_OP_ADD, s) GP_BIN(GP_OP_SUB, s) GP_BIN(GP_OP_MUL, s) GP_BIN(GP_OP_DIV, s)          \
-  GP_BIN(GP_OP_MIN, s) GP_BIN(GP_OP_MAX, s) GP_BIN(GP_OP_POW, s)
+#define GP_CONST(w) __uint_as_float(w)
+#define GP_ROWS(stmt) _Pragma("unroll") for (int r = 0; r < R; ++r) { stmt; }
 
+#define GP_PUSH(s)                                                                             \
+  case LBL(OPV_PUSH_V, s): { GP_FETCH_VAR(st[s], cw.y) } break;                                \
+  case LBL(OPV_PUSH_C, s): { const float c = GP_CONST(cw.y); GP_ROWS(st[s][r] = c) } break;
+
+// binary op OP at destination slot s; a = first operand, b = second operand
+#define GP_BIN_SS(OP, s)                                                                       \
+  case LBL(opv_bin(OP, BV_SS), s): { GP_ROWS(st[s][r] = apply2<OP>(st[(s) + 1][r], st[s][r])) } break;
+#define GP_BIN_T(OP, s)                                                                        \
+  case LBL(opv_bin(OP, BV_SV), s): { float t[R]; GP_FETCH_VAR(t, cw.z)                        \
+    GP_ROWS(st[s][r] = apply2<OP>(st[s][r], t[r])) } break;                                    \
+  case LBL(opv_bin(OP, BV_SC), s): { const float c = GP_CONST(cw.z);                           \
+    GP_ROWS(st[s][r] = apply2<OP>(st[s][r], c)) } break;                                       \
+  case LBL(opv_bin(OP, BV_VS), s): { float t[R]; GP_FETCH_VAR(t, cw.y)                         \
+    GP_ROWS(st[s][r] = apply2<OP>(t[r], st[s][r])) } break;                                    \
+  case LBL(opv_bin(OP, BV_CS), s): { const float c = GP_CONST(cw.y);                           \
+    GP_ROWS(st[s][r] = apply2<OP>(c, st[s][r])) } break;                                       \
+  case LBL(opv_bin(OP, BV_VV), s): { float t[R], u[R]; GP_FETCH_VAR(t, cw.y)                   \
+    GP_FETCH_VAR(u, cw.z) GP_ROWS(st[s][r] = apply2<OP>(t[r], u[r])) } break;                  \
+  case LBL(opv_bin(OP, BV_VC), s): { float t[R]; GP_FETCH_VAR(t, cw.y)                         \
+    const float c = GP_CONST(cw.z); GP_ROWS(st[s][r] = apply2<OP>(t[r], c)) } break;           \
+  case LBL(opv_bin(OP, BV_CV), s): { float u[R]; GP_FETCH_VAR(u, cw.z)                         \
+    const float c = GP_CONST(cw.y); GP_ROWS(st[s][r] = apply2<OP>(c, u[r])) } break;           \
+  case LBL(opv_bin(OP, BV_CC), s): {                                                           \
+    const float v = apply2<OP>(GP_CONST(cw.y), GP_CONST(cw.z)); GP_ROWS(st[s][r] = v) } break;
+#define GP_UN(OP, s)                                                                           \
+  case LBL(opv_un(OP, UV_S), s): { GP_ROWS(st[s][r] = apply1<OP>(st[s][r])) } break;           \
+  case LBL(opv_un(OP, UV_V), s): { float t[R]; GP_FETCH_VAR(t, cw.y)                           \
+    GP_ROWS(st[s][r] = apply1<OP>(t[r])) } break;                                              \
+  case LBL(opv_un(OP, UV_C), s): { const float v = apply1<OP>(GP_CONST(cw.y));                 \
+    GP_ROWS(st[s][r] = v) } break;
+
+#define GP_EACH_BIN(M, s)                                                                      \
+  M(GP_OP_ADD, s) M(GP_OP_SUB, s) M(GP_OP_MUL, s) M(GP_OP_DIV, s) M(GP_OP_MIN, s)              \
+  M(GP_OP_MAX, s) M(GP_OP_POW, s)
+#define GP_EACH_UN(M, s)                                                                       \
+  M(GP_OP_SIN, s) M(GP_OP_COS, s) M(GP_OP_TAN, s) M(GP_OP_ABS, s) M(GP_OP_NEG, s)              \
+  M(GP_OP_SQRT, s) M(GP_OP_LOG, s) M(GP_OP_EXP, s) M(GP_OP_INV, s) M(GP_OP_SQUARE, s)          \
+  M(GP_OP_CUBE, s) M(GP_OP_TANH, s) M(GP_OP_SINH, s) M(GP_OP_COSH, s) M(GP_OP_ASIN, s)         \
+  M(GP_OP_ACOS, s) M(GP_OP_ATAN, s)
+// every case whose destination slot is s (SS needs slot s + 1 as well)
+#define GP_SLOT_TU(s) GP_PUSH(s) GP_EACH_BIN(GP_BIN_T, s) GP_EACH_UN(GP_UN, s)
+#define GP_SLOT_B(s) GP_EACH_BIN(GP_BIN_SS, s)
+
+#define GP_FOR_0_2(M) M(0) M(1) M(2)
 #define GP_FOR_0_6(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6)
 #define GP_FOR_8_10(M) M(8) M(9) M(10)
 #define GP_FOR_12_18(M) M(12) M(13) M(14) M(15) M(16) M(17) M(18)
-#if GP_STACK == 8
+#if GP_STACK == 4
+#define GP_ALL_CASES GP_FOR_0_2(GP_SLOT_TU) GP_SLOT_TU(3) GP_FOR_0_2(GP_SLOT_B)
+#elif GP_STACK == 8
 #define GP_ALL_CASES GP_FOR_0_6(GP_SLOT_TU) GP_SLOT_TU(7) GP_FOR_0_6(GP_SLOT_B)
 #elif GP_STACK == 12
 #define GP_ALL_CASES                                                                           \
@@ -111,7 +143,7 @@ __host__ __device__ inline size_t smem_bytes(int G, int S, int n_cols, bool xsme
   GP_FOR_12_18(GP_SLOT_TU) GP_SLOT_TU(19)                                                      \
   GP_FOR_0_6(GP_SLOT_B) GP_SLOT_B(7) GP_FOR_8_10(GP_SLOT_B) GP_SLOT_B(11) GP_FOR_12_18(GP_SLOT_B)
 #else
-#error "GP_STACK must be 8, 12 or 20"
+#error "GP_STACK must be 4, 8, 12 or 20"
 #endif
 
 template <int M> struct MTag { static constexpr int value = M; };
@@ -128,51 +160,79 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 }
 
 template <bool PREDICT, bool XSMEM>
-__global__ void __launch_bounds__(NT) eval_kernel(const EvalArgs a) {
+__global__ void __launch_bounds__(NT, GP_MINB) eval_kernel(const EvalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_item;
   const int S = (a.metric == GP_PEARSON) ? 3 : 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int q = blockIdx.x, g = blockIdx.y;
-  const int p0 = g * a.G;
-  const int np = min(a.G, a.n_programs - p0);
+  const int count = *a.prog_count;                 // programs in this variant's bucket
+  const int n_groups = (count + a.G - 1) / a.G;
+  const int64_t n_items = (int64_t)n_groups * a.n_chunks;
   double* acc = reinterpret_cast<double*>(smem);                 // [NW][G][S]
-  double* cacc = acc + (size_t)NW * a.G * S;                     // [NW][3] dataset constants
   float* ys = reinterpret_cast<float*>(smem + (PREDICT ? 0 : smem_acc_bytes(a.G, S)));
   float* ws = ys + TILE;
   float* xs = ws + TILE;                                         // [n_cols][TILE] if XSMEM
-  const bool do_consts = !PREDICT && g == 0;
-
-  if constexpr (!PREDICT) {
-    for (int i = tid; i < NW * a.G * S + NW * 3; i += NT) acc[i] = 0.0;
-  }
+  const bool has_w = a.w != nullptr;
   const float Ky = (!PREDICT && S == 3) ? *a.y_shift : 0.0f;
 
-  const int64_t r_begin = (int64_t)q * a.rows_per_chunk;
-  const int64_t r_end = min(r_begin + a.rows_per_chunk, a.n_rows);
-
-  for (int64_t t0 = r_begin; t0 < r_end; t0 += TILE) {
-    const int nvalid = (int)min((int64_t)TILE, r_end - t0);
-    __syncthreads();  // previous tile's smem reads are done
-    // ---- A2: stage the tile (coalesced; padded rows get w = 0 -> skipped) -------------------
-    for (int i = tid; i < TILE; i += NT) {
-      const bool in = i < nvalid;
-      const int64_t row = t0 + i;
-      if constexpr (!PREDICT) {
-        ys[i] = in ? a.y[row] : 0.0f;
-        ws[i] = in ? (a.w ? a.w[row] : 1.0f) : 0.0f;
-      }
-      if constexpr (XSMEM) {
-        for (int c = 0; c < a.n_cols; ++c) xs[c * TILE + i] = in ? a.X[(int64_t)c * a.ldx + row] : 0.0f;
-      }
-    }
+  // Persistent CTAs pull work items (program group g fastest, then row chunk q) from a queue;
+  // each item's results go to fixed partial slots, so the sums do not depend on scheduling.
+  for (;;) {
+    __syncthreads();                               // previous item fully done with smem / s_item
+    if (tid == 0) s_item = atomicAdd(a.work_counter, 1);
     __syncthreads();
+    const int64_t item = s_item;
+    if (item >= n_items) break;
+    const int g = (int)(item % n_groups);
+    const int64_t q = item / n_groups;
+    const int np = min(a.G, count - g * a.G);
+    const int64_t s_begin = a.gstart[g], s_len = a.gstart[g + 1] - s_begin;
+    if constexpr (!PREDICT) {
+      for (int i = tid; i < NW * a.G * S; i += NT) acc[i] = 0.0;
+    }
+    const int64_t r_begin = q * a.rows_per_chunk;
+    const int64_t r_end = min(r_begin + a.rows_per_chunk, a.n_rows);
 
-    // ---- dataset constants W, S_y, S_yy (program independent; group 0 only) ----------------
-    if (do_consts) {
-      float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+    for (int64_t t0 = r_begin; t0 < r_end; t0 += TILE) {
+      const int nvalid = (int)min((int64_t)TILE, r_end - t0);
+      __syncthreads();  // previous tile's smem reads are done
+      // ---- A2: stage the tile (coalesced; padded rows get w = 0 -> skipped) -----------------
+      for (int i = tid; i < TILE; i += NT) {
+        const bool in = i < nvalid;
+        const int64_t row = t0 + i;
+        if constexpr (!PREDICT) {
+          ys[i] = in ? a.y[row] : 0.0f;
+          ws[i] = in ? (has_w ? a.w[row] : 1.0f) : 0.0f;
+        }
+        if constexpr (XSMEM) {
+          for (int c = 0; c < a.n_cols; ++c)
+            xs[c * TILE + i] = in ? a.X[(int64_t)c * a.ldx + row] : 0.0f;
+        }
+      }
+      __syncthreads();
+
+      // ---- A3 + A4 + A5: walk the group's code stream --------------------------------------
+      const uint4* __restrict__ sp = a.stream + s_begin;
+      int ebase = tid * 4;                           // element e(r) = ebase + (r/4)*NT*4 + r%4
+      float l0 = 0.f, l1 = 0.f, l2 = 0.f;
+      float st[STACK][R];
+      // fused weighted loss of the current pass's rows (A4)
+      auto loss = [&](auto tag, float Kp) {
+        constexpr int M = decltype(tag)::value;
+        if (M == GP_MSE && !has_w && nvalid == TILE) {
+          // unweighted full tile: every row is live, w = 1
 #pragma unroll
-      for (int sub = 0; sub < SUB; ++sub) {
-        const int ebase = sub * NT * R + tid * 4;
+          for (int k = 0; k < R4; ++k) {
+            const float4 yv = *reinterpret_cast<const float4*>(ys + ebase + k * NT * 4);
+            const float yy[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float d = st[0][4 * k + j] - yy[j];
+              l0 = fmaf(d, d, l0);
+            }
+          }
+          return;
+        }
 #pragma unroll
         for (int k = 0; k < R4; ++k) {
           const float4 yv = *reinterpret_cast<const float4*>(ys + ebase + k * NT * 4);
@@ -180,141 +240,119 @@ __global__ void __launch_bounds__(NT) eval_kernel(const EvalArgs a) {
           const float yy[4] = {yv.x, yv.y, yv.z, yv.w}, ww[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const float yc = yy[j] - Ky;
-            if (ww[j] != 0.0f) { c0 += ww[j]; c1 += ww[j] * yc; c2 += ww[j] * yc * yc; }
+            const float yh = st[0][4 * k + j];
+            const bool live = ww[j] != 0.0f;         // w = 0 rows are skipped, never multiplied
+            if constexpr (M == GP_MSE) {
+              const float d = yh - yy[j];
+              l0 += live ? ww[j] * d * d : 0.0f;
+            } else if constexpr (M == GP_MAE) {
+              l0 += live ? ww[j] * fabsf(yh - yy[j]) : 0.0f;
+            } else if constexpr (M == GP_LOGLOSS) {
+              // -[y ln p + (1-y) ln(1-p)], p = sigmoid(yh), y in {0,1}: softplus(-+yh),
+              // clamped to the p-clamp's range (C7)
+              const float z = yy[j] > 0.5f ? -yh : yh;
+              float l = fmaxf(z, 0.0f) + __logf(1.0f + __expf(-fabsf(z)));
+              l = l < kLogLossLo ? kLogLossLo : (l > kLogLossHi ? kLogLossHi : l);
+              l0 += live ? ww[j] * l : 0.0f;
+            } else {  // Pearson: shifted sums (C9)
+              const float d = yh - Kp, yc = yy[j] - Ky, wd = ww[j] * d;
+              l0 += live ? wd : 0.0f;
+              l1 += live ? wd * d : 0.0f;
+              l2 += live ? wd * yc : 0.0f;
+            }
           }
         }
-      }
-      const double d0 = warp_sum_f64(c0), d1 = warp_sum_f64(c1), d2 = warp_sum_f64(c2);
-      if (lane == 0) { cacc[warp * 3] += d0; cacc[warp * 3 + 1] += d1; cacc[warp * 3 + 2] += d2; }
-    }
-
-    // ---- A3 + A4 + A5 per program ----------------------------------------------------------
-    for (int pl = 0; pl < np; ++pl) {
-      const int p = p0 + pl;
-      const int len = a.code_len[p];
-      if (len == 0) continue;                       // invalid program (stage flags say why)
-      const uint2* __restrict__ pc = a.code + a.code_off[p];
-      const float Kp = (!PREDICT && S == 3) ? a.shift[p] : 0.0f;
-      float l0 = 0.f, l1 = 0.f, l2 = 0.f;
-#pragma unroll 1
-      for (int sub = 0; sub < SUB; ++sub) {
-        const int ebase = sub * NT * R + tid * 4;   // element e(r) = ebase + (r/4)*NT*4 + r%4
-        float st[STACK][R];
-        // two-deep software prefetch of the (warp-uniform) code words
-        uint2 nxt = __ldg(pc), nxt2 = __ldg(pc + 1);
-#pragma unroll 1
-        for (int kk = 0; kk < len; ++kk) {
-          const uint2 cw = nxt;
-          nxt = nxt2;
-          nxt2 = __ldg(pc + kk + 2);                // code buffer carries two pad words
-          switch (cw.x & kCaseMask) {
-            GP_ALL_CASES
-            default: __builtin_unreachable();  // stage kernel guarantees a valid (op, slot)
-          }
-        }
+      };
+      // end of one row pass of program p: prediction store or loss
+      auto end_pass = [&](const uint4& cw) {
         if constexpr (PREDICT) {
-          float* o = a.out + (int64_t)p * a.ld_out + t0;
+          float* o = a.out + (int64_t)cw.y * a.ld_out + t0;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const int e = ebase + (r >> 2) * NT * 4 + (r & 3);
             if (e < nvalid) o[e] = st[0][r];
           }
         } else {
-          // fused weighted loss, one uniform metric branch per pass (A4)
-          auto loss = [&](auto tag) {
-            constexpr int M = decltype(tag)::value;
-#pragma unroll
-            for (int k = 0; k < R4; ++k) {
-              const float4 yv = *reinterpret_cast<const float4*>(ys + ebase + k * NT * 4);
-              const float4 wv = *reinterpret_cast<const float4*>(ws + ebase + k * NT * 4);
-              const float yy[4] = {yv.x, yv.y, yv.z, yv.w}, ww[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float yh = st[0][4 * k + j];
-                const bool live = ww[j] != 0.0f;    // w = 0 rows are skipped, never multiplied
-                if constexpr (M == GP_MSE) {
-                  const float d = yh - yy[j];
-                  l0 += live ? ww[j] * d * d : 0.0f;
-                } else if constexpr (M == GP_MAE) {
-                  l0 += live ? ww[j] * fabsf(yh - yy[j]) : 0.0f;
-                } else if constexpr (M == GP_LOGLOSS) {
-                  // -[y ln p + (1-y) ln(1-p)], p = sigmoid(yh), y in {0,1}: softplus(-+yh),
-                  // clamped to the p-clamp's range (C7)
-                  const float z = yy[j] > 0.5f ? -yh : yh;
-                  float l = fmaxf(z, 0.0f) + __logf(1.0f + __expf(-fabsf(z)));
-                  l = l < kLogLossLo ? kLogLossLo : (l > kLogLossHi ? kLogLossHi : l);
-                  l0 += live ? ww[j] * l : 0.0f;
-                } else {  // Pearson: shifted sums (C9)
-                  const float d = yh - Kp, yc = yy[j] - Ky, wd = ww[j] * d;
-                  l0 += live ? wd : 0.0f;
-                  l1 += live ? wd * d : 0.0f;
-                  l2 += live ? wd * yc : 0.0f;
-                }
-              }
-            }
-          };
+          const float Kp = __uint_as_float(cw.w);
           switch (a.metric) {
-            case GP_MAE: loss(MTag<GP_MAE>{}); break;
-            case GP_MSE: case GP_RMSE: loss(MTag<GP_MSE>{}); break;
-            case GP_LOGLOSS: loss(MTag<GP_LOGLOSS>{}); break;
-            default: loss(MTag<GP_PEARSON>{}); break;
+            case GP_MAE: loss(MTag<GP_MAE>{}, Kp); break;
+            case GP_MSE: case GP_RMSE: loss(MTag<GP_MSE>{}, Kp); break;
+            case GP_LOGLOSS: loss(MTag<GP_LOGLOSS>{}, Kp); break;
+            default: loss(MTag<GP_PEARSON>{}, Kp); break;
           }
         }
-      }
-      if constexpr (!PREDICT) {
-        double* slot = acc + ((size_t)warp * a.G + pl) * S;
-        if (S == 1) {
-          const float v = warp_sum_f32(l0);
-          if (lane == 0) slot[0] += (double)v;
-        } else {
-          const double v0 = warp_sum_f64(l0), v1 = warp_sum_f64(l1), v2 = warp_sum_f64(l2);
-          if (lane == 0) { slot[0] += v0; slot[1] += v1; slot[2] += v2; }
+      };
+      // two-deep software prefetch of the (warp-uniform) stream words, uninterrupted across
+      // program boundaries
+      uint4 nxt = __ldg(sp), nxt2 = __ldg(sp + 1);
+#pragma unroll 1
+      for (int64_t kk = 0; kk < s_len; ++kk) {
+        const uint4 cw = nxt;
+        nxt = nxt2;
+        nxt2 = __ldg(sp + kk + 2);                   // stream buffer carries two pad words
+        switch (cw.x >> 2) {                         // .x = case id * 4 (jump-table offset)
+          GP_ALL_CASES
+          case kCaseEndPass: {                       // next row pass of the same program
+            end_pass(cw);
+            ebase = (int)cw.z * NT * R + tid * 4;
+          } break;
+          case kCaseEnd: {                           // program done: warp-reduce into smem (A5)
+            end_pass(cw);
+            if constexpr (!PREDICT) {
+              double* slot = acc + ((size_t)warp * a.G + cw.z) * S;
+              if (S == 1) {
+                const float v = warp_sum_f32(l0);
+                if (lane == 0) slot[0] += (double)v;
+              } else {
+                const double v0 = warp_sum_f64(l0), v1 = warp_sum_f64(l1), v2 = warp_sum_f64(l2);
+                if (lane == 0) { slot[0] += v0; slot[1] += v1; slot[2] += v2; }
+              }
+              l0 = l1 = l2 = 0.f;
+            }
+            ebase = tid * 4;
+          } break;
+          default: __builtin_unreachable();          // stage / pack guarantee a valid case
         }
       }
     }
-  }
 
-  if constexpr (!PREDICT) {
-    __syncthreads();
-    double* prow = a.partial + (int64_t)q * a.ld_part;
-    for (int j = tid; j < np * S; j += NT) {
-      const int pl = j / S, k = j - pl * S;
-      double s = 0.0;
-      for (int wv = 0; wv < NW; ++wv) s += acc[((size_t)wv * a.G + pl) * S + k];
-      prow[(int64_t)(p0 + pl) * S + k] = s;
-    }
-    if (g == 0 && tid < 3) {
-      double s = 0.0;
-      for (int wv = 0; wv < NW; ++wv) s += cacc[wv * 3 + tid];
-      prow[(int64_t)a.n_programs * S + tid] = s;
+    if constexpr (!PREDICT) {
+      __syncthreads();
+      double* prow = a.partial + q * a.ld_part;
+      const int32_t* __restrict__ ids = a.prog_ids + (int64_t)g * a.G;
+      for (int j = tid; j < np * S; j += NT) {
+        const int pl = j / S, k = j - pl * S;
+        double sum = 0.0;
+        for (int wv = 0; wv < NW; ++wv) sum += acc[((size_t)wv * a.G + pl) * S + k];
+        prow[(int64_t)ids[pl] * S + k] = sum;
+      }
     }
   }
 }
 
 template <bool P, bool XS>
-static cudaError_t launch_t(const EvalArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
+static cudaError_t launch_t(const EvalArgs& a, int n_ctas, size_t smem, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(eval_kernel<P, XS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  eval_kernel<P, XS><<<grid, NT, smem, s>>>(a);
+  eval_kernel<P, XS><<<n_ctas, NT, smem, s>>>(a);
   return cudaGetLastError();
 }
 
-static cudaError_t launch(const EvalArgs& a, bool predict, bool xsmem, dim3 grid, size_t smem,
+static cudaError_t launch(const EvalArgs& a, bool predict, bool xsmem, int n_ctas, size_t smem,
                           cudaStream_t s) {
-  if (predict) return xsmem ? launch_t<true, true>(a, grid, smem, s) : launch_t<true, false>(a, grid, smem, s);
-  return xsmem ? launch_t<false, true>(a, grid, smem, s) : launch_t<false, false>(a, grid, smem, s);
+  if (predict) return xsmem ? launch_t<true, true>(a, n_ctas, smem, s) : launch_t<true, false>(a, n_ctas, smem, s);
+  return xsmem ? launch_t<false, true>(a, n_ctas, smem, s) : launch_t<false, false>(a, n_ctas, smem, s);
 }
 
 template <bool P, bool XS>
 static int occ_t(size_t smem) {
   int n = 0;
-  cudaFuncSetAttribute(eval_kernel<P, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncSetAttribute(eval_kernel<P, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, eval_kernel<P, XS>, NT, smem);
   return n;
 }

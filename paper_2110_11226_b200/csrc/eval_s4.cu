@@ -1,0 +1,7 @@
+// Evaluator variant: register stack of 4 slots, 16 rows per thread per pass, 1 pass per tile.
+#define GP_STACK 4
+#define GP_R 16
+#define GP_SUB 1
+#define GP_NT 128
+#define GP_MINB 3
+#include "eval_impl.cuh"

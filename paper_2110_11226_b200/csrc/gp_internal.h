@@ -23,10 +23,9 @@ struct EvalPlan {
 };
 
 bool is_host_pointer(const void* p);
-const EvalVariant& pick_variant(int max_stack);
 int sm_count(int device);
-EvalPlan plan_eval(const EvalVariant& v, int device, int64_t n_rows, int32_t n_programs,
-                   int32_t n_cols, int S, bool predict);
+EvalPlan plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t n_cols, int S,
+                   bool predict);
 
 }  // namespace gpb
 
@@ -36,7 +35,8 @@ struct gp_context {
   void* comm = nullptr;  // ncclComm_t
   std::string err;
   // device workspaces (grown on demand, stream-ordered)
-  gpb::StageBuf code, code_off, code_len, status, partial, sums, shift, xref;
+  gpb::StageBuf code, code_off, code_len, need, lists, pos, gstart, counts, codestream, status, partial,
+      sums, shift, xref;
   // staging for [host] arguments
   gpb::StageBuf h_nodes, h_off, h_X, h_y, h_w, h_fit;
   std::vector<float> xref_host;
@@ -49,7 +49,8 @@ struct gp_context {
   int64_t prof_launches = 0;
 
   std::vector<gpb::StageBuf*> all_buffers() {
-    return {&code, &code_off, &code_len, &status, &partial, &sums, &shift, &xref,
+    return {&code, &code_off, &code_len, &need, &lists, &pos, &gstart, &counts, &codestream, &status,
+            &partial, &sums, &shift, &xref,
             &h_nodes, &h_off, &h_X, &h_y, &h_w, &h_fit};
   }
   gp_status fail(gp_status s, const char* fmt, ...);

@@ -7,11 +7,33 @@
 
 namespace gpb {
 
-// Everything the fused evaluator needs for one launch (see eval_impl.cuh).
+// Case ids of the compiled code use ONE slot stride for every evaluator variant (so the stage
+// kernel is variant independent): case id = opv * kCaseStride + slot.
+constexpr int kCaseStride = GP_MAX_STACK;
+// Row tile of every variant (NT * R * SUB = 2048) -> one work decomposition for all variants.
+constexpr int kTile = 2048;
+// Evaluator variants by register-stack capacity; program p runs in the first variant whose
+// capacity >= its stack need (bucketed on the device, no host synchronisation).
+constexpr int kNumVariants = 4;
+constexpr int kVariantStack[kNumVariants] = {4, 8, 12, 20};
+
+// Passes per program per tile of each variant (rows = NT * R * pass).
+constexpr int kVariantSub[kNumVariants] = {1, 2, 4, 4};
+// Stream marker cases (after every (op, variant, slot) case id).
+constexpr int kCaseEndPass = 116 * kCaseStride;   // OPV_COUNT * kCaseStride
+constexpr int kCaseEnd = kCaseEndPass + 1;
+
+// Everything the fused evaluator needs for one launch (see eval_impl.cuh). Each variant runs a
+// packed CODE STREAM per program group: for every program of the group, SUB copies of its code
+// words (one per row pass) each followed by a marker word -- END_PASS {case, p, next pass, K_p} or
+// END {case, p, index within the group, K_p} -- so the evaluator walks one contiguous stream with
+// an uninterrupted prefetch and does the loss / reduction in the marker cases.
 struct EvalArgs {
-  const uint2* code;          // compiled nodes, evaluation order, +2 pad words
-  const int64_t* code_off;    // [n_programs] start of each program in code
-  const int32_t* code_len;    // [n_programs] length, 0 = invalid (skipped)
+  const uint4* stream;        // this variant's packed stream (+2 pad words)
+  const int64_t* gstart;      // [n_groups + 1] stream offsets of the program groups
+  const int32_t* prog_ids;    // [count] program index of each bucket slot (the bucket list)
+  const int32_t* prog_count;  // device: number of programs in the bucket
+  int32_t* work_counter;      // device: persistent-CTA work queue (zeroed by the bucket kernel)
   const float* X;             // column-major, X[c * ldx + i]
   int64_t ldx;
   const float* y;             // [n_rows] (FIT mode)
@@ -20,17 +42,17 @@ struct EvalArgs {
   int32_t n_cols;
   int32_t n_programs;
   int32_t metric;             // gp_metric
-  int32_t G;                  // programs per group (grid.y = ceil(n_programs / G))
-  int64_t rows_per_chunk;     // rows per work item (grid.x = ceil(n_rows / rows_per_chunk))
-  double* partial;            // FIT: [grid.x][ld_part], ld_part = n_programs * S + 3
+  int32_t G;                  // programs per group
+  int64_t rows_per_chunk;     // rows per work item (multiple of kTile)
+  int64_t n_chunks;           // row chunks; work items = ceil(count / G) * n_chunks
+  double* partial;            // FIT: [n_chunks][ld_part], ld_part = n_programs * S + 3
   int64_t ld_part;
-  const float* shift;         // Pearson: K_p per program (nullptr otherwise)
   const float* y_shift;       // Pearson: device scalar K_y
   float* out;                 // PREDICT: out[p * ld_out + i]
   int64_t ld_out;
 };
 
-// Static shape of one evaluator variant (chosen by max stack need).
+// Static shape of one evaluator variant.
 struct EvalShape {
   int stack;                  // register-stack capacity
   int R;                      // rows per thread per pass
@@ -39,25 +61,43 @@ struct EvalShape {
   int tile() const { return NT * R * SUB; }
 };
 
-// Per-capacity evaluator translation units (eval_s8.cu, eval_s12.cu, eval_s20.cu).
+// Per-capacity evaluator translation units (eval_s4.cu, eval_s8.cu, eval_s12.cu, eval_s20.cu).
 struct EvalVariant {
   EvalShape shape;
-  // Launches the evaluator; xsmem selects X staged in shared memory (small n_cols) versus
-  // per-node L1/L2 loads (large n_cols). Returns the CUDA error of the launch.
-  cudaError_t (*launch)(const EvalArgs& a, bool predict, bool xsmem, dim3 grid, size_t smem,
+  // Launches the persistent evaluator with n_ctas CTAs; xsmem selects X staged in shared memory
+  // (small n_cols) versus per-node L1/L2 loads (large n_cols).
+  cudaError_t (*launch)(const EvalArgs& a, bool predict, bool xsmem, int n_ctas, size_t smem,
                         cudaStream_t s);
   // Resident CTAs per SM for the given dynamic shared memory.
   int (*occupancy)(bool predict, bool xsmem, size_t smem);
 };
+const EvalVariant& eval_variant_s4();
 const EvalVariant& eval_variant_s8();
 const EvalVariant& eval_variant_s12();
 const EvalVariant& eval_variant_s20();
 
 // aux.cu
 cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n_programs,
-                         int64_t n_nodes, int32_t n_cols, int32_t stack_cap, uint2* code,
-                         int64_t* code_off, int32_t* code_len, uint32_t* status, cudaStream_t s);
-cudaError_t launch_shift(const uint2* code, const int64_t* code_off, const int32_t* code_len,
+                         int64_t n_nodes, int32_t n_cols, int32_t max_stack, uint4* code,
+                         int64_t* code_off, int32_t* code_len, int32_t* need, uint32_t* status,
+                         cudaStream_t s);
+// Partitions valid programs by stack need into kNumVariants ascending lists, lays out each
+// variant's code stream (per-program offsets, group starts for G programs per group), zeroes the
+// work counters. lists/pos: [kNumVariants][n_programs]; gstart: [kNumVariants][n_programs + 1];
+// counts: [kNumVariants] then counters [kNumVariants]; base: [kNumVariants + 1] stream bases.
+cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
+                          int32_t G, int32_t* lists, int64_t* pos, int64_t* gstart,
+                          int32_t* counts, int64_t* base, cudaStream_t s);
+// Copies every bucketed program's code into its variant stream with the pass / end markers.
+cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
+                        const int32_t* lists, const int64_t* pos, const int32_t* counts,
+                        const int64_t* base, const float* shift, int32_t n_programs, int32_t G,
+                        uint4* stream, cudaStream_t s);
+// Dataset constants W, S_y, S_yy per row chunk -> partial[q][col0 .. col0 + 2].
+cudaError_t launch_consts(const float* y, const float* w, int64_t n_rows, int64_t rows_per_chunk,
+                          int64_t n_chunks, const float* y_shift, double* partial, int64_t ld_part,
+                          int64_t col0, cudaStream_t s);
+cudaError_t launch_shift(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                          int32_t n_programs, int32_t stack_cap, const float* xref,
                          int64_t xref_stride, float* shift_out, cudaStream_t s);
 cudaError_t launch_tile_reduce(const double* partial, int64_t n_chunks, int64_t ld_part,

@@ -64,14 +64,18 @@ def check_fitness(gpu_fit, ref, sens, flags, metric, max_excluded=0.03):
     # Pearson r lies in [-1, 1]: fp32 accumulation over >= 1e3 rows gives absolute errors of
     # order 1e-8 independent of |r|, so its floor is absolute (1e-4 * 1e-2 = 1e-6 on r).
     floor = 1e-2 if metric == "pearson" else 1e-6
-    excluded = 0
+    excluded = undefined_nonzero = 0
     for p in range(len(ref)):
         if flags[p] & F_INV:
             assert gpu_fit[p] == (-math.inf if metric == "pearson" else math.inf), p
             continue
         r, g = ref[p], float(gpu_fit[p])
         if flags[p] & F_UND and not flags[p] & (F_OVF | F_AMB):
-            assert g == 0.0, (p, g)          # constant program: Pearson undefined -> 0 (C4)
+            # constant in double: Pearson undefined -> 0 (C4). In fp32 such a program can vary by
+            # rounding ((x + 1) - x), and the GPU then reports r of its fp32 values: counted.
+            assert abs(g) <= 1.0, (p, g)
+            if g != 0.0:
+                undefined_nonzero += 1
             continue
         if flags[p] & (F_OVF | F_AMB) or not math.isfinite(sens[p]):
             excluded += 1                    # no usable error bound: reported, not compared
@@ -82,6 +86,7 @@ def check_fitness(gpu_fit, ref, sens, flags, metric, max_excluded=0.03):
         tol = 1e-4 * max(abs(r), floor) + 4 * sens[p] + abs(r) * 2 ** -23
         assert abs(g - r) <= tol, f"program {p}: gpu {g!r} ref {r!r} tol {tol!r} sens {sens[p]!r}"
     assert excluded <= max_excluded * len(ref) + 1, excluded
+    assert undefined_nonzero <= 0.02 * len(ref) + 1, undefined_nonzero
 
 
 # ---- execution step (gp_predict) ---------------------------------------------------------------
@@ -215,6 +220,15 @@ def test_determinism(gp, ctx):
 
 
 # ---- edge cases --------------------------------------------------------------------------------
+def full_tree(orc, depth):
+    """Full binary add-tree of the given depth: with terminal operands folded into their parents
+    the evaluator still needs `depth` stack slots (both operands of every inner node are values)."""
+    if depth == 0:
+        return orc.program(("var", 0))
+    sub = full_tree(orc, depth - 1)
+    return np.concatenate([orc.program("add"), sub, sub])
+
+
 def test_edge_cases(gp, ctx, orc):
     P = orc.program
     progs = [
@@ -223,7 +237,7 @@ def test_edge_cases(gp, ctx, orc):
         P("add", ("var", 0)),                                   # dangling -> invalid
         P(("var", 0), ("var", 1)),                              # underflow -> invalid
         P(("var", 5)),                                          # var out of range
-        P("add", "add", "add", "add", "add", "add", "add", "add", *([("var", 0)] * 9)),  # need 9
+        full_tree(orc, 9),                                      # stack need 9 > 8
         P("div", ("var", 0), "sub", ("var", 1), ("var", 1)),    # protected division by 0
     ]
     nodes = np.concatenate(progs)
