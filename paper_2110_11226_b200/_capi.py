@@ -5,7 +5,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgp_b200.so")
+# GP_B200_LIB overrides the library path (experiments: alternative kernel shapes)
+LIB_PATH = os.environ.get("GP_B200_LIB", os.path.join(HERE, "libgp_b200.so"))
 
 P = ctypes.c_void_p
 i32, i64, u32, u64, f32, f64 = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64,

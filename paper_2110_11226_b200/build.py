@@ -7,6 +7,7 @@ from __future__ import annotations
 import concurrent.futures as cf
 import glob
 import os
+import re
 import subprocess
 import sys
 
@@ -28,9 +29,17 @@ CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-I", os.path.join(CUDA, "in
              "-I", os.path.join(ROOT, "include")]
 
 
-def _headers():
-    return glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
-        [os.path.join(ROOT, "include", "gp.h")]
+def _deps(path, seen=None):
+    """The file and every header it (transitively) #includes with quotes."""
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    for line in open(path):
+        m = re.match(r'\s*#\s*include\s+"([^"]+)"', line)
+        if m:
+            _deps(os.path.normpath(os.path.join(os.path.dirname(path), m.group(1))), seen)
+    return seen
 
 
 def _stale(target, deps):
@@ -42,7 +51,7 @@ def _stale(target, deps):
 
 def _compile(src, force):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    if not force and not _stale(obj, [src] + _headers()):
+    if not force and not _stale(obj, sorted(_deps(src))):
         return obj, None
     if src.endswith(".cu"):
         cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]

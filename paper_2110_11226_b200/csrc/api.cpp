@@ -357,14 +357,16 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   }
   int32_t* counts = (int32_t*)ctx->counts.p;
   int64_t* base = (int64_t*)(counts + 2 * kNumVariants);
+  int subs[kNumVariants];  // row passes per program of each variant (its compiled shape)
+  for (int v = 0; v < kNumVariants; ++v) subs[v] = variant(v).shape.SUB;
   if ((s = ctx->cuda(launch_bucket((const int32_t*)ctx->need.p, (const int32_t*)ctx->code_len.p,
-                                   n_programs, G, (int32_t*)ctx->lists.p, (int64_t*)ctx->pos.p,
+                                   n_programs, G, subs, (int32_t*)ctx->lists.p, (int64_t*)ctx->pos.p,
                                    (int64_t*)ctx->gstart.p, counts, base, ctx->stream),
                      "bucket kernel"))) return s;
   return ctx->cuda(launch_pack((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
                                (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->lists.p,
                                (const int64_t*)ctx->pos.p, counts, base, shift, n_programs, G,
-                               (uint4*)ctx->codestream.p, ctx->stream),
+                               subs, (uint4*)ctx->codestream.p, ctx->stream),
                    "pack kernel");
 }
 

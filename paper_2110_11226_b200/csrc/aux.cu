@@ -6,7 +6,7 @@
 //   select     (A8) Philox tournament selection with parsimony
 #include <cfloat>
 #include "device_ops.cuh"
-#include "kernels.h"
+#include "aux.h"
 
 namespace gpb {
 
@@ -153,13 +153,13 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
                                                       int64_t* __restrict__ pos,
                                                       int64_t* __restrict__ gstart,
                                                       int32_t* __restrict__ counts,
-                                                      int64_t* __restrict__ base) {
+                                                      int64_t* __restrict__ base, int4 sub4) {
   __shared__ int warp_cnt[kNumVariants][32];
   __shared__ int cnt[kNumVariants];
   __shared__ int64_t warp_tot[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int caps[kNumVariants] = {4, 8, 12, 20};   // kVariantStack
-  const int subs[kNumVariants] = {1, 2, 4, 4};     // kVariantSub
+  const int subs[kNumVariants] = {sub4.x, sub4.y, sub4.z, sub4.w};  // row passes per variant
   if (tid < kNumVariants) { cnt[tid] = 0; counts[kNumVariants + tid] = 0; }  // work counters
   __syncthreads();
   // phase 1: stable partition by stack need
@@ -215,10 +215,10 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
 }
 
 cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
-                          int32_t G, int32_t* lists, int64_t* pos, int64_t* gstart,
-                          int32_t* counts, int64_t* base, cudaStream_t s) {
+                          int32_t G, const int* subs, int32_t* lists, int64_t* pos,
+                          int64_t* gstart, int32_t* counts, int64_t* base, cudaStream_t s) {
   bucket_kernel<<<1, 1024, 0, s>>>(need, code_len, n_programs, G, lists, pos, gstart, counts,
-                                   base);
+                                   base, make_int4(subs[0], subs[1], subs[2], subs[3]));
   return cudaGetLastError();
 }
 
@@ -228,13 +228,13 @@ __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __res
                             const int32_t* __restrict__ code_len, const int32_t* __restrict__ lists,
                             const int64_t* __restrict__ pos, const int32_t* __restrict__ counts,
                             const int64_t* __restrict__ base, const float* __restrict__ shift,
-                            int32_t n, int32_t G, uint4* __restrict__ stream) {
+                            int32_t n, int32_t G, int4 sub4, uint4* __restrict__ stream) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) stream[base[kNumVariants]] = stream[base[kNumVariants] + 1] = make_uint4(0, 0, 0, 0);
   if (i >= (int64_t)kNumVariants * n) return;
   const int b = (int)(i / n), j = (int)(i % n);
   if (j >= counts[b]) return;
-  const int subs[kNumVariants] = {1, 2, 4, 4};
+  const int subs[kNumVariants] = {sub4.x, sub4.y, sub4.z, sub4.w};
   const int p = lists[i];
   const int len = code_len[p];
   const uint4* src = code + code_off[p];
@@ -251,12 +251,15 @@ __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __res
 cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                         const int32_t* lists, const int64_t* pos, const int32_t* counts,
                         const int64_t* base, const float* shift, int32_t n_programs, int32_t G,
-                        uint4* stream, cudaStream_t s) {
+                        const int* subs, uint4* stream, cudaStream_t s) {
   const int nt = 256;
   const int64_t total = (int64_t)kNumVariants * n_programs;
   pack_kernel<<<(unsigned)((total + nt - 1) / nt), nt, 0, s>>>(code, code_off, code_len, lists,
                                                                pos, counts, base, shift,
-                                                               n_programs, G, stream);
+                                                               n_programs, G,
+                                                               make_int4(subs[0], subs[1], subs[2],
+                                                                         subs[3]),
+                                                               stream);
   return cudaGetLastError();
 }
 

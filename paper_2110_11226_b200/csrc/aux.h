@@ -1,0 +1,43 @@
+// aux.h -- launchers of the small kernels in aux.cu (stage, bucket/layout, pack, shift, consts,
+// tile reduce, finalize, select). Included by aux.cu and the host layer only, so the evaluator
+// translation units do not depend on it.
+#pragma once
+#include "kernels.h"
+
+namespace gpb {
+
+// aux.cu
+cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n_programs,
+                         int64_t n_nodes, int32_t n_cols, int32_t max_stack, uint4* code,
+                         int64_t* code_off, int32_t* code_len, int32_t* need, uint32_t* status,
+                         cudaStream_t s);
+// Partitions valid programs by stack need into kNumVariants ascending lists, lays out each
+// variant's code stream (per-program offsets, group starts for G programs per group), zeroes the
+// work counters. lists/pos: [kNumVariants][n_programs]; gstart: [kNumVariants][n_programs + 1];
+// counts: [kNumVariants] then counters [kNumVariants]; base: [kNumVariants + 1] stream bases.
+cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
+                          int32_t G, const int* subs, int32_t* lists, int64_t* pos,
+                          int64_t* gstart, int32_t* counts, int64_t* base, cudaStream_t s);
+// Copies every bucketed program's code into its variant stream with the pass / end markers.
+cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
+                        const int32_t* lists, const int64_t* pos, const int32_t* counts,
+                        const int64_t* base, const float* shift, int32_t n_programs, int32_t G,
+                        const int* subs, uint4* stream, cudaStream_t s);
+// Dataset constants W, S_y, S_yy per row chunk -> partial[q][col0 .. col0 + 2].
+cudaError_t launch_consts(const float* y, const float* w, int64_t n_rows, int64_t rows_per_chunk,
+                          int64_t n_chunks, const float* y_shift, double* partial, int64_t ld_part,
+                          int64_t col0, cudaStream_t s);
+cudaError_t launch_shift(const uint4* code, const int64_t* code_off, const int32_t* code_len,
+                         int32_t n_programs, int32_t stack_cap, const float* xref,
+                         int64_t xref_stride, float* shift_out, cudaStream_t s);
+cudaError_t launch_tile_reduce(const double* partial, int64_t n_chunks, int64_t ld_part,
+                               double* sums, cudaStream_t s);
+cudaError_t launch_finalize(const double* sums, int32_t n_programs, int32_t metric,
+                            const int32_t* code_len, float* fitness, uint32_t* status,
+                            cudaStream_t s);
+cudaError_t launch_select(const float* fitness, const int64_t* offsets, int32_t n_programs,
+                          int32_t n_tournaments, int32_t k, float parsimony, int32_t higher,
+                          uint64_t seed, uint32_t generation, int32_t* winners, cudaStream_t s);
+cudaError_t launch_copy_scalar(const float* src, float* dst, cudaStream_t s);
+
+}  // namespace gpb

@@ -65,51 +65,65 @@ __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
 #define LBL(OPV, s) ((OPV) * kCaseStride + (s))
 
 // -- dispatch cases -------------------------------------------------------------------------------
-// Operand fetch of a variable into R registers: from the shared-memory tile (LDS.128 per 4 rows)
-// or, for wide datasets, from global memory through L1/L2 (rows clamped into the tile).
-#define GP_FETCH_VAR(t, var)                                                                   \
+// Cases work on 4-row chunks (one LDS.128 of a variable per chunk), so a fused variable operand
+// needs 4 temporary registers, not R: register pressure sets the occupancy of this latency-bound
+// kernel. GP_VAR4(v, var, k) loads rows 4k..4k+3 of variable `var` into float4 v: from the
+// shared-memory tile, or (wide datasets) from global memory through L1/L2 with rows clamped into
+// the tile.
+#define GP_VAR4(v, var, k)                                                                     \
+  float4 v;                                                                                    \
   if constexpr (XSMEM) {                                                                       \
-    const float4* xv = reinterpret_cast<const float4*>(xs + (int)(var) * TILE + ebase);        \
-    _Pragma("unroll") for (int k = 0; k < R4; ++k) {                                           \
-      const float4 v = xv[k * NT];                                                             \
-      t[4 * k] = v.x; t[4 * k + 1] = v.y; t[4 * k + 2] = v.z; t[4 * k + 3] = v.w;              \
-    }                                                                                          \
+    v = reinterpret_cast<const float4*>(xs + (int)(var) * TILE + ebase)[(k) * NT];             \
   } else {                                                                                     \
-    const float* xv = a.X + (int64_t)(var) * a.ldx + t0;                                       \
-    _Pragma("unroll") for (int r = 0; r < R; ++r)                                              \
-      t[r] = __ldg(xv + min(ebase + (r >> 2) * NT * 4 + (r & 3), nvalid - 1));                 \
+    const float* xv_ = a.X + (int64_t)(var) * a.ldx + t0;                                      \
+    const int e_ = ebase + (k) * NT * 4;                                                       \
+    v.x = __ldg(xv_ + min(e_, nvalid - 1));                                                    \
+    v.y = __ldg(xv_ + min(e_ + 1, nvalid - 1));                                                \
+    v.z = __ldg(xv_ + min(e_ + 2, nvalid - 1));                                                \
+    v.w = __ldg(xv_ + min(e_ + 3, nvalid - 1));                                                \
   }
 #define GP_CONST(w) __uint_as_float(w)
 #define GP_ROWS(stmt) _Pragma("unroll") for (int r = 0; r < R; ++r) { stmt; }
+// for each 4-row chunk k: stmt4(j) applied to rows r = 4k + j
+#define GP_CHUNKS(pre, stmt)                                                                   \
+  _Pragma("unroll") for (int k = 0; k < R4; ++k) {                                             \
+    pre;                                                                                       \
+    { const int r = 4 * k;     const int j_ = 0; (void)j_; stmt; }                             \
+    { const int r = 4 * k + 1; const int j_ = 1; (void)j_; stmt; }                             \
+    { const int r = 4 * k + 2; const int j_ = 2; (void)j_; stmt; }                             \
+    { const int r = 4 * k + 3; const int j_ = 3; (void)j_; stmt; }                             \
+  }
+#define GP_F4(v) (j_ == 0 ? v.x : j_ == 1 ? v.y : j_ == 2 ? v.z : v.w)
 
 #define GP_PUSH(s)                                                                             \
-  case LBL(OPV_PUSH_V, s): { GP_FETCH_VAR(st[s], cw.y) } break;                                \
+  case LBL(OPV_PUSH_V, s): { GP_CHUNKS(GP_VAR4(t, cw.y, k), st[s][r] = GP_F4(t)) } break;      \
   case LBL(OPV_PUSH_C, s): { const float c = GP_CONST(cw.y); GP_ROWS(st[s][r] = c) } break;
 
 // binary op OP at destination slot s; a = first operand, b = second operand
 #define GP_BIN_SS(OP, s)                                                                       \
   case LBL(opv_bin(OP, BV_SS), s): { GP_ROWS(st[s][r] = apply2<OP>(st[(s) + 1][r], st[s][r])) } break;
 #define GP_BIN_T(OP, s)                                                                        \
-  case LBL(opv_bin(OP, BV_SV), s): { float t[R]; GP_FETCH_VAR(t, cw.z)                        \
-    GP_ROWS(st[s][r] = apply2<OP>(st[s][r], t[r])) } break;                                    \
+  case LBL(opv_bin(OP, BV_SV), s): {                                                           \
+    GP_CHUNKS(GP_VAR4(t, cw.z, k), st[s][r] = apply2<OP>(st[s][r], GP_F4(t))) } break;         \
   case LBL(opv_bin(OP, BV_SC), s): { const float c = GP_CONST(cw.z);                           \
     GP_ROWS(st[s][r] = apply2<OP>(st[s][r], c)) } break;                                       \
-  case LBL(opv_bin(OP, BV_VS), s): { float t[R]; GP_FETCH_VAR(t, cw.y)                         \
-    GP_ROWS(st[s][r] = apply2<OP>(t[r], st[s][r])) } break;                                    \
+  case LBL(opv_bin(OP, BV_VS), s): {                                                           \
+    GP_CHUNKS(GP_VAR4(t, cw.y, k), st[s][r] = apply2<OP>(GP_F4(t), st[s][r])) } break;         \
   case LBL(opv_bin(OP, BV_CS), s): { const float c = GP_CONST(cw.y);                           \
     GP_ROWS(st[s][r] = apply2<OP>(c, st[s][r])) } break;                                       \
-  case LBL(opv_bin(OP, BV_VV), s): { float t[R], u[R]; GP_FETCH_VAR(t, cw.y)                   \
-    GP_FETCH_VAR(u, cw.z) GP_ROWS(st[s][r] = apply2<OP>(t[r], u[r])) } break;                  \
-  case LBL(opv_bin(OP, BV_VC), s): { float t[R]; GP_FETCH_VAR(t, cw.y)                         \
-    const float c = GP_CONST(cw.z); GP_ROWS(st[s][r] = apply2<OP>(t[r], c)) } break;           \
-  case LBL(opv_bin(OP, BV_CV), s): { float u[R]; GP_FETCH_VAR(u, cw.z)                         \
-    const float c = GP_CONST(cw.y); GP_ROWS(st[s][r] = apply2<OP>(c, u[r])) } break;           \
+  case LBL(opv_bin(OP, BV_VV), s): {                                                           \
+    GP_CHUNKS(GP_VAR4(t, cw.y, k) GP_VAR4(u, cw.z, k),                                         \
+              st[s][r] = apply2<OP>(GP_F4(t), GP_F4(u))) } break;                              \
+  case LBL(opv_bin(OP, BV_VC), s): { const float c = GP_CONST(cw.z);                           \
+    GP_CHUNKS(GP_VAR4(t, cw.y, k), st[s][r] = apply2<OP>(GP_F4(t), c)) } break;                \
+  case LBL(opv_bin(OP, BV_CV), s): { const float c = GP_CONST(cw.y);                           \
+    GP_CHUNKS(GP_VAR4(u, cw.z, k), st[s][r] = apply2<OP>(c, GP_F4(u))) } break;                \
   case LBL(opv_bin(OP, BV_CC), s): {                                                           \
     const float v = apply2<OP>(GP_CONST(cw.y), GP_CONST(cw.z)); GP_ROWS(st[s][r] = v) } break;
 #define GP_UN(OP, s)                                                                           \
   case LBL(opv_un(OP, UV_S), s): { GP_ROWS(st[s][r] = apply1<OP>(st[s][r])) } break;           \
-  case LBL(opv_un(OP, UV_V), s): { float t[R]; GP_FETCH_VAR(t, cw.y)                           \
-    GP_ROWS(st[s][r] = apply1<OP>(t[r])) } break;                                              \
+  case LBL(opv_un(OP, UV_V), s): {                                                             \
+    GP_CHUNKS(GP_VAR4(t, cw.y, k), st[s][r] = apply1<OP>(GP_F4(t))) } break;                   \
   case LBL(opv_un(OP, UV_C), s): { const float v = apply1<OP>(GP_CONST(cw.y));                 \
     GP_ROWS(st[s][r] = v) } break;
 
@@ -160,7 +174,9 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 }
 
 template <bool PREDICT, bool XSMEM>
-__global__ void __launch_bounds__(NT, GP_MINB) eval_kernel(const EvalArgs a) {
+// the global-X instantiation holds more live addresses: one resident CTA less
+__global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB - 1 : 1))
+    eval_kernel(const EvalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_item;
   const int S = (a.metric == GP_PEARSON) ? 3 : 1;

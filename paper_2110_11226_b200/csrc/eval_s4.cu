@@ -3,5 +3,5 @@
 #define GP_R 16
 #define GP_SUB 1
 #define GP_NT 128
-#define GP_MINB 3
+#define GP_MINB 5
 #include "eval_impl.cuh"

@@ -6,7 +6,7 @@
 #include <vector>
 
 #include "../../include/gp.h"
-#include "kernels.h"
+#include "aux.h"
 
 namespace gpb {
 
