@@ -166,7 +166,9 @@ def run_b200(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     uid = None
-    if world > 1:
+    if world > 1 or args.nccl:
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         obj = [gp.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
@@ -191,6 +193,7 @@ def run_b200(args, cfg):
     # ---- timed region: K generations, inputs resident in HBM -----------------------------------
     ctx.set_profiling(True)
     ctx.eval_timing(reset=True)
+    ctx.kernel_launches(reset=True)
     steps = []
     with ClockSampler(local) as clk:
         barrier()
@@ -204,6 +207,7 @@ def run_b200(args, cfg):
         barrier()
     ms = e0.elapsed_time(e1)
     eval_ms, eval_launches = ctx.eval_timing(reset=True)
+    launches = ctx.kernel_launches(reset=True)
     ctx.set_profiling(False)
     node_evals = sum(s["total_nodes"] for s in steps) * m_global
     t = torch.tensor([ms, eval_ms], dtype=torch.float64, device=f"cuda:{local}")
@@ -275,14 +279,14 @@ def run_b200(args, cfg):
                        "parallelism": f"rows sharded over {world} GPU(s)",
                        "l2": "inputs larger than L2 (X + y = %.0f MB)" % ((Xh.nbytes + yh.nbytes) * world / 1e6)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(sum(5 + (2 if cfg["metric"] == "pearson" else 0) for _ in steps)),
+            "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "phases_ms_per_step": {k: round(1e3 * float(np.mean([s[k] for s in steps])), 3)
                                    for k in ("t_select_s", "t_mutate_s", "t_h2d_s", "t_eval_s")},
         }
     eng.close()
     ctx.close()
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return out
 
@@ -342,6 +346,8 @@ def main():
     ap.add_argument("--weak", action="store_true", help="per-GPU rows fixed (default: strong)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nccl", action="store_true",
+                    help="use the NCCL communicator path even with one rank (plumbing check)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

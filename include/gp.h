@@ -110,8 +110,9 @@ const char* gp_version(void);
 gp_status gp_get_unique_id(void* out_id);
 
 /* Creates a context on `device`, issuing work on `stream` (a cudaStream_t; NULL = legacy default
- * stream). nccl_unique_id [host]: NULL for a single GPU; otherwise the 128-byte id from
- * gp_get_unique_id, and every rank 0 <= rank < world_size must call this collectively. With
+ * stream). nccl_unique_id [host]: NULL for a single GPU without a communicator; otherwise the
+ * 128-byte id from gp_get_unique_id, and every rank 0 <= rank < world_size must call this
+ * collectively (world_size 1 with an id creates a one-rank communicator). With
  * world_size > 1 each rank passes its own contiguous row shard to gp_evaluate, and the
  * per-program partial sums are combined with one fp64 ncclAllReduce per evaluation, so every
  * rank receives bit-identical fitness. */
@@ -133,6 +134,8 @@ gp_status gp_context_set_reference_row(gp_context* ctx, const float* x_ref, int3
  * recorded events]. */
 gp_status gp_context_set_profiling(gp_context* ctx, int enabled);
 gp_status gp_context_eval_timing(gp_context* ctx, double* total_ms, int64_t* launches, int reset);
+/* Number of CUDA kernels this context has launched (all entry points) since the last reset. */
+gp_status gp_context_kernel_launches(gp_context* ctx, int64_t* launches, int reset);
 
 /* ---------------------------------------------------------------------------------------------
  * gp_evaluate -- Evaluate + fitness of a whole population (Alg. 1 line 7).

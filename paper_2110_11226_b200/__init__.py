@@ -126,6 +126,13 @@ class Context:
                                             int(reset)), self.handle, "eval_timing")
         return ms.value, n.value
 
+    def kernel_launches(self, reset: bool = True) -> int:
+        """CUDA kernels launched by the library on this context since the last reset."""
+        n = ctypes.c_int64()
+        _check(lib().gp_context_kernel_launches(self.handle, ctypes.byref(n), int(reset)),
+               self.handle, "kernel_launches")
+        return n.value
+
     def set_reference_row(self, x_row, y_ref: float):
         x = np.ascontiguousarray(np.asarray(x_row, np.float32))
         _check(lib().gp_context_set_reference_row(self.handle, x.ctypes.data, len(x),

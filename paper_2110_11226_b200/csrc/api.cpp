@@ -67,6 +67,11 @@ gp_status gp_context::cuda(cudaError_t e, const char* what) {
               cudaGetErrorString(e));
 }
 
+gp_status gp_context::launch(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) ++kernel_launches;
+  return cuda(e, what);
+}
+
 gp_status gp_context::grow(void** p, size_t* cap, size_t bytes, const char* what) {
   if (*cap >= bytes && *p) return GP_OK;
   if (*p) cudaFreeAsync(*p, stream);
@@ -165,7 +170,7 @@ static gp_status launch_variants(gp_context* ctx, EvalArgs a, const EvalPlan& pl
     a.prog_count = (const int32_t*)ctx->counts.p + v;
     a.work_counter = (int32_t*)ctx->counts.p + kNumVariants + v;
     const int occ = std::max(1, var.occupancy(predict, pl.xsmem, pl.smem));
-    gp_status s = ctx->cuda(var.launch(a, predict, pl.xsmem, ctx->sms * occ, pl.smem, ctx->stream),
+    gp_status s = ctx->launch(var.launch(a, predict, pl.xsmem, ctx->sms * occ, pl.smem, ctx->stream),
                             predict ? "predict kernel" : "eval kernel");
     if (s) return s;
   }
@@ -224,7 +229,7 @@ gp_status gp_context_create(gp_context** out, int device, void* stream, const vo
   c->rank = rank;
   c->world = world_size;
   c->sms = sm_count(device);
-  if (world_size > 1) {
+  if (nccl_unique_id) {
     NcclApi& n = nccl();
     if (!n.ok) { delete c; g_last_global_error = "libnccl.so.2 could not be loaded"; return GP_ERR_NCCL; }
     ncclUniqueId id;
@@ -284,6 +289,13 @@ gp_status gp_context_eval_timing(gp_context* ctx, double* total_ms, int64_t* lau
   return GP_OK;
 }
 
+gp_status gp_context_kernel_launches(gp_context* ctx, int64_t* launches, int reset) {
+  if (!ctx) return GP_ERR_ARG;
+  if (launches) *launches = ctx->kernel_launches;
+  if (reset) ctx->kernel_launches = 0;
+  return GP_OK;
+}
+
 gp_status gp_context_set_reference_row(gp_context* ctx, const float* x_ref, int32_t n_cols,
                                        float y_ref) {
   if (!ctx || !x_ref || n_cols < 1) return GP_ERR_ARG;
@@ -330,7 +342,7 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   // stream words <= SUB_max x (code words + one marker per program) + 2 pad words
   if ((s = ctx->grow(&ctx->codestream.p, &ctx->codestream.cap, ((size_t)4 * (n_nodes + n) + 2) * sizeof(uint4), "stream"))) return s;
   if ((s = ctx->grow(&ctx->status.p, &ctx->status.cap, (size_t)n * sizeof(uint32_t), "status"))) return s;
-  if ((s = ctx->cuda(launch_stage(programs, offsets, n_programs, n_nodes, n_cols, max_stack,
+  if ((s = ctx->launch(launch_stage(programs, offsets, n_programs, n_nodes, n_cols, max_stack,
                                   (uint4*)ctx->code.p, (int64_t*)ctx->code_off.p,
                                   (int32_t*)ctx->code_len.p, (int32_t*)ctx->need.p,
                                   (uint32_t*)ctx->status.p, ctx->stream), "stage kernel"))) return s;
@@ -349,8 +361,8 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
       stride = ldx;
       yref = y;
     }
-    if ((s = ctx->cuda(launch_copy_scalar(yref, sh + n, ctx->stream), "y shift"))) return s;
-    if ((s = ctx->cuda(launch_shift((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
+    if ((s = ctx->launch(launch_copy_scalar(yref, sh + n, ctx->stream), "y shift"))) return s;
+    if ((s = ctx->launch(launch_shift((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
                                     (const int32_t*)ctx->code_len.p, n_programs, kCaseStride,
                                     xref, stride, sh, ctx->stream), "shift kernel"))) return s;
     shift = sh;
@@ -359,11 +371,11 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   int64_t* base = (int64_t*)(counts + 2 * kNumVariants);
   int subs[kNumVariants];  // row passes per program of each variant (its compiled shape)
   for (int v = 0; v < kNumVariants; ++v) subs[v] = variant(v).shape.SUB;
-  if ((s = ctx->cuda(launch_bucket((const int32_t*)ctx->need.p, (const int32_t*)ctx->code_len.p,
+  if ((s = ctx->launch(launch_bucket((const int32_t*)ctx->need.p, (const int32_t*)ctx->code_len.p,
                                    n_programs, G, subs, (int32_t*)ctx->lists.p, (int64_t*)ctx->pos.p,
                                    (int64_t*)ctx->gstart.p, counts, base, ctx->stream),
                      "bucket kernel"))) return s;
-  return ctx->cuda(launch_pack((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
+  return ctx->launch(launch_pack((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
                                (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->lists.p,
                                (const int64_t*)ctx->pos.p, counts, base, shift, n_programs, G,
                                subs, (uint4*)ctx->codestream.p, ctx->stream),
@@ -416,14 +428,14 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
   a.ld_part = ld_part;
   a.y_shift = metric == GP_PEARSON ? (const float*)ctx->shift.p + n_programs : nullptr;
   ctx->last_plan = pl;
-  if ((s = ctx->cuda(launch_consts(y, w, n_rows, pl.rows_per_chunk, pl.n_chunks, a.y_shift,
+  if ((s = ctx->launch(launch_consts(y, w, n_rows, pl.rows_per_chunk, pl.n_chunks, a.y_shift,
                                    a.partial, ld_part, (int64_t)n_programs * S, ctx->stream),
                      "consts kernel"))) return s;
   if ((s = launch_variants(ctx, a, pl, max_stack, false))) return s;
-  if ((s = ctx->cuda(launch_tile_reduce((const double*)ctx->partial.p, pl.n_chunks, ld_part,
+  if ((s = ctx->launch(launch_tile_reduce((const double*)ctx->partial.p, pl.n_chunks, ld_part,
                                         (double*)ctx->sums.p, ctx->stream), "tile_reduce"))) return s;
   // A6: one all-reduce of the fp64 partial sums across ranks (rows are sharded)
-  if (ctx->world > 1) {
+  if (ctx->comm) {
     NcclApi& n = nccl();
     ncclResult_t r = n.AllReduce(ctx->sums.p, ctx->sums.p, (size_t)ld_part, ncclFloat64, ncclSum,
                                  (ncclComm_t)ctx->comm, ctx->stream);
@@ -435,7 +447,7 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
     if ((s = ctx->grow(&ctx->h_fit.p, &ctx->h_fit.cap, (size_t)n_programs * sizeof(float), "fit"))) return s;
     fit_dev = (float*)ctx->h_fit.p;
   }
-  if ((s = ctx->cuda(launch_finalize((const double*)ctx->sums.p, n_programs, metric,
+  if ((s = ctx->launch(launch_finalize((const double*)ctx->sums.p, n_programs, metric,
                                      (const int32_t*)ctx->code_len.p, fit_dev,
                                      (uint32_t*)ctx->status.p, ctx->stream), "finalize"))) return s;
   if (fit_host) {
@@ -497,7 +509,7 @@ gp_status gp_tournament_select(gp_context* ctx, const float* fitness, const int6
       tournament_size < 1)
     return ctx->fail(GP_ERR_ARG, "invalid tournament arguments (n=%d T=%d k=%d)", n_programs,
                      n_tournaments, tournament_size);
-  return ctx->cuda(launch_select(fitness, node_offsets, n_programs, n_tournaments, tournament_size,
+  return ctx->launch(launch_select(fitness, node_offsets, n_programs, n_tournaments, tournament_size,
                                  parsimony, higher_is_better ? 1 : 0, seed, generation,
                                  winners_out, ctx->stream), "select kernel");
 }

@@ -47,6 +47,7 @@ struct gp_context {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
   double prof_ms = 0.0;
   int64_t prof_launches = 0;
+  int64_t kernel_launches = 0;   // gp_context_kernel_launches
 
   std::vector<gpb::StageBuf*> all_buffers() {
     return {&code, &code_off, &code_len, &need, &lists, &pos, &gstart, &counts, &codestream, &status,
@@ -55,6 +56,7 @@ struct gp_context {
   }
   gp_status fail(gp_status s, const char* fmt, ...);
   gp_status cuda(cudaError_t e, const char* what);
+  gp_status launch(cudaError_t e, const char* what);  // cuda() + counts a successful launch
   gp_status grow(void** p, size_t* cap, size_t bytes, const char* what);
   gp_status stage_in(const void* src, size_t bytes, gpb::StageBuf& buf, const void** dst,
                      bool* was_host);

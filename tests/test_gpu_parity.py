@@ -292,3 +292,16 @@ def test_tournament_win_law(gp, ctx):
     cnt = np.bincount(w.cpu().numpy(), minlength=3)
     expect = 1e6 * np.array([3 / 9, 5 / 9, 1 / 9])
     assert ((cnt - expect) ** 2 / expect).sum() < 13.8
+
+
+# ---- NCCL plumbing on one GPU: a one-rank communicator's all-reduce is an exact identity ----------
+def test_single_rank_nccl_context_matches(gp, ctx):
+    X, y = synth.pagie_grid(50)
+    nodes, off = synth.random_population(100, seed=31, depth=(1, 6), max_stack=8)
+    c1 = gp.Context(0, unique_id=gp.get_unique_id(), rank=0, world_size=1)
+    for metric in ("mse", "pearson"):
+        a, sa = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric=metric, max_stack=8)
+        b, sb = c1.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric=metric, max_stack=8)
+        assert torch.equal(a, b) and torch.equal(sa, sb)
+    assert c1.kernel_launches() > 0
+    c1.close()
