@@ -134,6 +134,12 @@ gp_status gp_context_set_reference_row(gp_context* ctx, const float* x_ref, int3
  * recorded events]. */
 gp_status gp_context_set_profiling(gp_context* ctx, int enabled);
 gp_status gp_context_eval_timing(gp_context* ctx, double* total_ms, int64_t* launches, int reset);
+/* Evaluation order of the compiled programs. 1 (default): for every binary node whose operands
+ * are both computed values, the operand needing more stack slots is evaluated first
+ * (Sethi-Ullman), which minimises the register-stack need; 0: the classic reverse-prefix order
+ * (second operand first). Results are identical either way (same operations on the same
+ * operands); only the stack need, hence the evaluator variant a program runs in, changes. */
+gp_status gp_context_set_eval_order(gp_context* ctx, int sethi_ullman);
 /* Number of CUDA kernels this context has launched (all entry points) since the last reset. */
 gp_status gp_context_kernel_launches(gp_context* ctx, int64_t* launches, int reset);
 
@@ -155,8 +161,11 @@ gp_status gp_context_kernel_launches(gp_context* ctx, int64_t* launches, int res
  *                node_offsets[n_programs] == n_nodes
  *  n_programs    >= 1
  *  n_nodes       [host] total node count
- *  max_stack     [host] bound on every program's stack need, 1..GP_MAX_STACK; selects the kernel
- *                variant. Programs needing more get GP_FLAG_STACK_OVERFLOW.
+ *  max_stack     [host] bound on every program's stack need, 1..GP_MAX_STACK. The evaluator keeps
+ *                only computed values on its register stack (terminal operands are folded into
+ *                their parent), so its need is <= the classic reverse-prefix need (and smaller
+ *                still with the Sethi-Ullman order, gp_context_set_eval_order). Programs needing
+ *                more than max_stack get GP_FLAG_STACK_OVERFLOW.
  *  X             [host|device] fp32, column-major: feature c of local row i at
  *                X[c * ldx + i]; ldx >= n_rows (ldx > n_rows lets a rank pass a row window of
  *                a global column-major array)

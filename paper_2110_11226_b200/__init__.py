@@ -126,6 +126,11 @@ class Context:
                                             int(reset)), self.handle, "eval_timing")
         return ms.value, n.value
 
+    def set_eval_order(self, sethi_ullman: bool = True):
+        """Sethi-Ullman operand order (default) or the classic reverse-prefix order."""
+        _check(lib().gp_context_set_eval_order(self.handle, int(bool(sethi_ullman))), self.handle,
+               "set_eval_order")
+
     def kernel_launches(self, reset: bool = True) -> int:
         """CUDA kernels launched by the library on this context since the last reset."""
         n = ctypes.c_int64()

@@ -117,12 +117,12 @@ int gpb::sm_count(int device) {
 // row chunk, about 8 items per resident CTA slot so the persistent CTAs' queue balances groups
 // of unequal total program length. All variants share the 2048-row tile.
 EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t n_cols, int S,
-                        bool predict) {
+                        bool predict, bool weighted) {
   EvalPlan pl;
   const int tile = kTile;
   const int64_t n_tiles = (n_rows + tile - 1) / tile;
   const int NW = 4;  // NT = 128 in every variant
-  const int g_max = 256;
+  const int g_max = 128;
   pl.xsmem = (size_t)n_cols * tile * sizeof(float) <= 96 * 1024;
   const int occ_guess = 4;
   const int64_t target = (int64_t)sm_count(device) * occ_guess * 8;
@@ -137,7 +137,9 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   pl.n_chunks = Q;
   pl.rows_per_chunk = tpc * tile;
   const size_t acc = predict ? 0 : (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15);
-  pl.smem = acc + 2 * (size_t)tile * sizeof(float) + (pl.xsmem ? (size_t)n_cols * tile * sizeof(float) : 0);
+  const size_t yw = predict ? 0 : (weighted ? 2 : 1) * (size_t)tile * sizeof(float);
+  pl.smem = acc + yw + (pl.xsmem ? (size_t)n_cols * tile * sizeof(float) : 0) +
+            (size_t)(kStreamWin + 2) * 16;
   return pl;
 }
 
@@ -289,6 +291,12 @@ gp_status gp_context_eval_timing(gp_context* ctx, double* total_ms, int64_t* lau
   return GP_OK;
 }
 
+gp_status gp_context_set_eval_order(gp_context* ctx, int sethi_ullman) {
+  if (!ctx) return GP_ERR_ARG;
+  ctx->sethi_ullman = sethi_ullman != 0;
+  return GP_OK;
+}
+
 gp_status gp_context_kernel_launches(gp_context* ctx, int64_t* launches, int reset) {
   if (!ctx) return GP_ERR_ARG;
   if (launches) *launches = ctx->kernel_launches;
@@ -342,10 +350,13 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   // stream words <= SUB_max x (code words + one marker per program) + 2 pad words
   if ((s = ctx->grow(&ctx->codestream.p, &ctx->codestream.cap, ((size_t)4 * (n_nodes + n) + 2) * sizeof(uint4), "stream"))) return s;
   if ((s = ctx->grow(&ctx->status.p, &ctx->status.cap, (size_t)n * sizeof(uint32_t), "status"))) return s;
+  if ((s = ctx->grow(&ctx->scratch.p, &ctx->scratch.cap, (size_t)2 * n_nodes * sizeof(int32_t), "scratch"))) return s;
   if ((s = ctx->launch(launch_stage(programs, offsets, n_programs, n_nodes, n_cols, max_stack,
                                   (uint4*)ctx->code.p, (int64_t*)ctx->code_off.p,
                                   (int32_t*)ctx->code_len.p, (int32_t*)ctx->need.p,
-                                  (uint32_t*)ctx->status.p, ctx->stream), "stage kernel"))) return s;
+                                  (uint32_t*)ctx->status.p, (int32_t*)ctx->scratch.p,
+                                  ctx->sethi_ullman ? 1 : 0, ctx->stream),
+                     "stage kernel"))) return s;
   const float* shift = nullptr;
   if (pearson) {  // DESIGN.md C9: K_p = f_p(reference row), K_y = y_ref
     if ((s = ctx->grow(&ctx->shift.p, &ctx->shift.cap, (size_t)n * sizeof(float) + 16, "shift"))) return s;
@@ -404,7 +415,7 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
   const bool fit_host = is_host_pointer(fitness_out);
   const bool st_host = status_out && is_host_pointer(status_out);
   const int S = metric == GP_PEARSON ? 3 : 1;
-  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, S, false);
+  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, S, false, w != nullptr);
   if ((s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, n_rows,
                    n_cols, pl.G, metric == GP_PEARSON, y, &any_host))) return s;
 
@@ -471,7 +482,7 @@ gp_status gp_predict(gp_context* ctx, const gp_node* programs, const int64_t* no
   cudaSetDevice(ctx->device);
   if (!out || ld_out < n_rows) return ctx->fail(GP_ERR_ARG, "invalid out / ld_out");
   bool any_host = false;
-  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, 1, true);
+  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, 1, true, false);
   gp_status s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx,
                         n_rows, n_cols, pl.G, false, nullptr, &any_host);
   if (s) return s;

@@ -13,24 +13,20 @@ namespace gpb {
 // ---------------------------------------------------------------------------------------------
 // Stage / compile. One thread per program (programs are short; a few µs total).
 //  - prefix validation with the needed-counter scan, opcode and variable-range checks
-//  - reverse (evaluation-order) walk that folds every terminal into its parent's code word
-//    and assigns the static destination slot of every emitted node (device_ops.cuh "compiled
-//    program code"); stack need = max occupancy; > capacity -> GP_FLAG_STACK_OVERFLOW
+//  - a bottom-up pass computes every subtree's stack need with terminals folded into their
+//    parent's code word and the Sethi-Ullman order (evaluate the child needing more slots first;
+//    the classic reverse-prefix order of P:194 is the default, swapped only when it needs more);
+//    a post-order emission then writes one code word per function node with its static
+//    destination slot (device_ops.cuh "compiled program code"); stack need > capacity ->
+//    GP_FLAG_STACK_OVERFLOW. Depth > 127 is also reported as overflow.
 // Invalid programs get code_len = 0 and are skipped by every later kernel.
 // ---------------------------------------------------------------------------------------------
-namespace {
-struct Operand {        // pending operand during the reverse walk
-  uint32_t kind;        // 0 stack value, 1 variable, 2 constant
-  uint32_t payload;     // variable index or fp32 bits
-};
-constexpr int kMaxPending = 64;
-}  // namespace
-
 __global__ void stage_kernel(const gp_node* __restrict__ nodes, const int64_t* __restrict__ off,
                              int32_t n_programs, int64_t n_nodes, int32_t n_cols, int32_t cap,
                              uint4* __restrict__ code, int64_t* __restrict__ code_off,
                              int32_t* __restrict__ code_len, int32_t* __restrict__ need_out,
-                             uint32_t* __restrict__ status) {
+                             uint32_t* __restrict__ status, int32_t* __restrict__ scratch,
+                             int32_t sethi_ullman) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p == 0) code[n_nodes] = code[n_nodes + 1] = make_uint4(0u, 0u, 0u, 0u);  // prefetch pads
   if (p >= n_programs) return;
@@ -51,52 +47,107 @@ __global__ void stage_kernel(const gp_node* __restrict__ nodes, const int64_t* _
     if (!(flags & GP_FLAG_BAD_OPCODE) && needed != 0) flags |= GP_FLAG_INVALID_PREFIX;
   }
   int64_t emitted = 0;
-  int need = 0;
+  int need_root = 0;
   if (!flags) {
-    Operand pend[kMaxPending];
-    int np = 0, sp = 0;
+    // (1) bottom-up (reverse prefix) pass: subtree end and stack need of every node, with
+    // terminals folded into their parents (need 0) and Sethi-Ullman child order for binary nodes
+    // whose operands are both stack values: evaluate the child needing more slots first.
+    int32_t* nd_need = scratch + b;               // per node
+    int32_t* nd_end = scratch + n_nodes + b;      // per node (relative to b)
+    const int64_t len = e - b;
+    for (int64_t i = len - 1; i >= 0; --i) {
+      const int a = op_arity(nodes[b + i].op);
+      if (a == 0) { nd_need[i] = 0; nd_end[i] = (int32_t)(i + 1); continue; }
+      const int64_t A = i + 1;
+      const int nA = nd_need[A];
+      if (a == 1) { nd_need[i] = nA > 0 ? nA : 1; nd_end[i] = nd_end[A]; continue; }
+      const int64_t B = nd_end[A];
+      const int nB = nd_need[B];
+      int n;
+      if (nA == 0 || nB == 0) n = max(max(nA, nB), 1);
+      else n = sethi_ullman ? min(max(nB, 1 + nA), max(nA, 1 + nB)) : max(nB, 1 + nA);
+      nd_need[i] = n;
+      nd_end[i] = nd_end[B];
+    }
+    need_root = len == 1 ? 1 : nd_need[0];
+    if (need_root > cap) flags |= GP_FLAG_STACK_OVERFLOW;
+  }
+  if (!flags) {
+    // (2) post-order emission with the chosen child order; terminal operands go into the word
+    const int32_t* nd_need = scratch + b;
+    const int32_t* nd_end = scratch + n_nodes + b;
+    auto src = [&](int64_t i, uint32_t* pl) -> int {  // 0 stack, 1 variable, 2 constant
+      const gp_node nd = nodes[b + i];
+      if (nd.op == GP_OP_VAR) { *pl = (uint32_t)nd.var; return 1; }
+      if (nd.op == GP_OP_CONST) { *pl = __float_as_uint(nd.value); return 2; }
+      *pl = 0u;
+      return 0;
+    };
     auto emit = [&](int opv, int slot, uint32_t pa, uint32_t pb) {
       code[b + emitted++] = make_uint4((uint32_t)(opv * kCaseStride + slot) * 4u, pa, pb, 0u);
     };
-    for (int64_t i = e - 1; i >= b && !flags; --i) {
-      const gp_node nd = nodes[i];
-      const int a = op_arity(nd.op);
-      if (a == 0) {
-        if (np == kMaxPending) { flags |= GP_FLAG_STACK_OVERFLOW; break; }
-        pend[np++] = Operand{nd.op == GP_OP_VAR ? 1u : 2u, nd.op == GP_OP_VAR ? (uint32_t)nd.var
-                                                                              : __float_as_uint(nd.value)};
-        continue;
-      }
-      if (a == 1) {
-        const Operand A = pend[--np];
-        int slot;
-        if (A.kind == 0) { slot = sp - 1; emit(opv_un(nd.op, UV_S), slot, 0u, 0u); }
-        else { slot = sp; emit(opv_un(nd.op, A.kind == 1 ? UV_V : UV_C), slot, A.payload, 0u); }
-        sp = slot + 1;
-      } else {
-        const Operand A = pend[--np];   // first pop = first operand
-        const Operand B = pend[--np];
-        int v, slot;
-        if (A.kind == 0 && B.kind == 0) { v = BV_SS; slot = sp - 2; }
-        else if (A.kind == 0) { v = B.kind == 1 ? BV_SV : BV_SC; slot = sp - 1; }
-        else if (B.kind == 0) { v = A.kind == 1 ? BV_VS : BV_CS; slot = sp - 1; }
-        else {
-          v = A.kind == 1 ? (B.kind == 1 ? BV_VV : BV_VC) : (B.kind == 1 ? BV_CV : BV_CC);
-          slot = sp;
+    if (e - b == 1) {
+      uint32_t pl;
+      const int k = src(0, &pl);
+      emit(k == 1 ? OPV_PUSH_V : OPV_PUSH_C, 0, pl, 0u);
+    } else {
+      constexpr int kMaxDepth = 128;
+      int64_t stk_i[kMaxDepth];
+      int stk_ph[kMaxDepth];
+      int top = 0, sp = 0;
+      stk_i[0] = 0;
+      stk_ph[0] = 0;
+      while (top >= 0) {
+        const int64_t i = stk_i[top];
+        const int ph = stk_ph[top];
+        const int ar = op_arity(nodes[b + i].op);
+        const int64_t A = i + 1, B = ar == 2 ? nd_end[A] : -1;
+        uint32_t pa, pb = 0u;
+        const int sa = src(A, &pa), sb = ar == 2 ? src(B, &pb) : -1;
+        // both operands on the stack: default order evaluates B first (reverse prefix);
+        // Sethi-Ullman swaps when that needs fewer slots
+        const bool both = ar == 2 && sa == 0 && sb == 0;
+        const bool a_first = both && sethi_ullman &&
+                             max(nd_need[A], 1 + nd_need[B]) < max(nd_need[B], 1 + nd_need[A]);
+        int64_t child = -1;
+        if (ph == 0) {
+          if (ar == 1) child = sa == 0 ? A : -1;
+          else if (both) child = a_first ? A : B;
+          else if (sa == 0) child = A;
+          else if (sb == 0) child = B;
+        } else if (ph == 1 && both) {
+          child = a_first ? B : A;
         }
-        emit(opv_bin(nd.op, v), slot, A.payload, B.payload);
-        sp = slot + 1;
+        if (child >= 0) {
+          stk_ph[top] = ph + 1;
+          if (top + 1 >= kMaxDepth) { flags |= GP_FLAG_STACK_OVERFLOW; break; }
+          ++top;
+          stk_i[top] = child;
+          stk_ph[top] = 0;
+          continue;
+        }
+        // all stack operands are evaluated: emit this node
+        const int op = nodes[b + i].op;
+        if (ar == 1) {
+          if (sa == 0) { emit(opv_un(op, UV_S), sp - 1, 0u, 0u); }
+          else { emit(opv_un(op, sa == 1 ? UV_V : UV_C), sp, pa, 0u); ++sp; }
+        } else if (both) {
+          sp -= 1;
+          emit(opv_bin(op, a_first ? BV_SSR : BV_SS), sp - 1, 0u, 0u);
+        } else if (sa == 0) {
+          emit(opv_bin(op, sb == 1 ? BV_SV : BV_SC), sp - 1, pa, pb);
+        } else if (sb == 0) {
+          emit(opv_bin(op, sa == 1 ? BV_VS : BV_CS), sp - 1, pa, pb);
+        } else {
+          const int v = sa == 1 ? (sb == 1 ? BV_VV : BV_VC) : (sb == 1 ? BV_CV : BV_CC);
+          emit(opv_bin(op, v), sp, pa, pb);
+          ++sp;
+        }
+        --top;
       }
-      pend[np++] = Operand{0u, 0u};
-      need = need > sp ? need : sp;
-      if (need > cap) flags |= GP_FLAG_STACK_OVERFLOW;
-    }
-    if (!flags && pend[0].kind != 0) {  // lone terminal program: one push
-      emit(pend[0].kind == 1 ? OPV_PUSH_V : OPV_PUSH_C, 0, pend[0].payload, 0u);
-      need = 1;
     }
   }
-  need_out[p] = need;
+  need_out[p] = need_root;
   code_off[p] = b;
   code_len[p] = flags ? 0 : (int32_t)emitted;
   status[p] = flags;
@@ -105,11 +156,12 @@ __global__ void stage_kernel(const gp_node* __restrict__ nodes, const int64_t* _
 cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n_programs,
                          int64_t n_nodes, int32_t n_cols, int32_t max_stack, uint4* code,
                          int64_t* code_off, int32_t* code_len, int32_t* need, uint32_t* status,
-                         cudaStream_t s) {
+                         int32_t* scratch, int32_t sethi_ullman, cudaStream_t s) {
   const int nt = 128;
   stage_kernel<<<(n_programs + nt - 1) / nt, nt, 0, s>>>(nodes, offsets, n_programs, n_nodes,
                                                           n_cols, max_stack, code, code_off,
-                                                          code_len, need, status);
+                                                          code_len, need, status, scratch,
+                                                          sethi_ullman);
   return cudaGetLastError();
 }
 
@@ -324,10 +376,11 @@ __global__ void shift_kernel(const uint4* __restrict__ code, const int64_t* __re
     if (opv < OPV_BIN0) {
       stk[slot] = term(opv == OPV_PUSH_V ? 1 : 2, cw.y);
     } else if (opv < OPV_UN0) {
-      const int op = GP_OP_ADD + (opv - OPV_BIN0) / 9, v = (opv - OPV_BIN0) % 9;
+      const int op = GP_OP_ADD + (opv - OPV_BIN0) / 10, v = (opv - OPV_BIN0) % 10;
       float a, bb;
       switch (v) {
         case BV_SS: a = stk[slot + 1]; bb = stk[slot]; break;
+        case BV_SSR: a = stk[slot]; bb = stk[slot + 1]; break;
         case BV_SV: case BV_SC: a = stk[slot]; bb = term(v == BV_SV ? 1 : 2, cw.z); break;
         case BV_VS: case BV_CS: a = term(v == BV_VS ? 1 : 2, cw.y); bb = stk[slot]; break;
         default:

@@ -175,15 +175,17 @@ __device__ __forceinline__ float apply_rt(int op, float a, float b) {
 //   .z = payload of the second operand b (variable index, or fp32 constant bits)
 // opv enumerates (op, operand-source variant) pairs:
 //   0 push var, 1 push const;
-//   binary op o (2..8): 2 + (o-2)*9 + v, v = SS, SV, SC, VS, CS, VV, VC, CV, CC
-//       (S = stack, V = variable, C = constant; first letter = operand a, second = operand b)
-//   unary op o (9..25): 65 + (o-9)*3 + u, u = S, V, C
+//   binary op o (2..8): 2 + (o-2)*10 + v, v = SS, SV, SC, VS, CS, VV, VC, CV, CC, SSR
+//       (S = stack, V = variable, C = constant; first letter = operand a, second = operand b;
+//        SSR = both on the stack with a evaluated FIRST -- Sethi-Ullman order)
+//   unary op o (9..25): 72 + (o-9)*3 + u, u = S, V, C
 // slot = destination stack slot (static: occupancy depends only on the tree shape):
-//   S,S -> a = st[slot+1], b = st[slot];  one S -> that operand is st[slot];  no S -> new slot.
-enum { OPV_PUSH_V = 0, OPV_PUSH_C = 1, OPV_BIN0 = 2, OPV_UN0 = 65, OPV_COUNT = 116 };
-enum { BV_SS = 0, BV_SV, BV_SC, BV_VS, BV_CS, BV_VV, BV_VC, BV_CV, BV_CC };
+//   SS -> a = st[slot+1], b = st[slot];  SSR -> a = st[slot], b = st[slot+1];
+//   one S -> that operand is st[slot];  no S -> new slot.
+enum { OPV_PUSH_V = 0, OPV_PUSH_C = 1, OPV_BIN0 = 2, OPV_UN0 = 72, OPV_COUNT = 123 };
+enum { BV_SS = 0, BV_SV, BV_SC, BV_VS, BV_CS, BV_VV, BV_VC, BV_CV, BV_CC, BV_SSR };
 enum { UV_S = 0, UV_V, UV_C };
-__host__ __device__ constexpr int opv_bin(int op, int v) { return OPV_BIN0 + (op - GP_OP_ADD) * 9 + v; }
+__host__ __device__ constexpr int opv_bin(int op, int v) { return OPV_BIN0 + (op - GP_OP_ADD) * 10 + v; }
 __host__ __device__ constexpr int opv_un(int op, int u) { return OPV_UN0 + (op - GP_OP_SIN) * 3 + u; }
 
 }  // namespace gpb

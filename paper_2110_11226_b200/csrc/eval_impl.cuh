@@ -37,6 +37,9 @@
 #ifndef GP_MINB
 #define GP_MINB 1   // minimum resident CTAs per SM (register budget = 64K / (GP_MINB * NT))
 #endif
+#ifndef GP_PREFETCH_CASE_ONLY
+#define GP_PREFETCH_CASE_ONLY 1   // 0: prefetch whole code words (more registers)
+#endif
 
 #define GP_CAT2(a, b) a##b
 #define GP_CAT(a, b) GP_CAT2(a, b)
@@ -53,11 +56,13 @@ static_assert(STACK <= kCaseStride, "slot must fit the case stride");
 
 // dynamic shared-memory opt-in: 227 KB per CTA minus the kernel's static shared memory
 constexpr int kMaxDynSmem = 220 * 1024;
+static_assert(kStreamWin % 4 == 0, "stream window");
 
 constexpr float kLogLossLo = 1.0000000000000005e-15f;  // -ln(1 - 1e-15), S:191 clamp (C7)
 constexpr float kLogLossHi = 34.538776394910684f;      // -ln(1e-15)
 
-// Shared-memory layout (bytes): fp64 accumulators [NW][G][S] | ys[TILE] | ws[TILE] | xs[n_cols][TILE]
+// Shared-memory layout (bytes): fp64 accumulators [NW][G][S] | ys[TILE] | ws[TILE] (weighted only)
+// | xs[n_cols][TILE] (small n_cols only) | code-stream window [kStreamWin + 2] uint4
 __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
   return ((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15;
 }
@@ -101,7 +106,8 @@ __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
 
 // binary op OP at destination slot s; a = first operand, b = second operand
 #define GP_BIN_SS(OP, s)                                                                       \
-  case LBL(opv_bin(OP, BV_SS), s): { GP_ROWS(st[s][r] = apply2<OP>(st[(s) + 1][r], st[s][r])) } break;
+  case LBL(opv_bin(OP, BV_SS), s): { GP_ROWS(st[s][r] = apply2<OP>(st[(s) + 1][r], st[s][r])) } break; \
+  case LBL(opv_bin(OP, BV_SSR), s): { GP_ROWS(st[s][r] = apply2<OP>(st[s][r], st[(s) + 1][r])) } break;
 #define GP_BIN_T(OP, s)                                                                        \
   case LBL(opv_bin(OP, BV_SV), s): {                                                           \
     GP_CHUNKS(GP_VAR4(t, cw.z, k), st[s][r] = apply2<OP>(st[s][r], GP_F4(t))) } break;         \
@@ -137,7 +143,7 @@ __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
   M(GP_OP_ACOS, s) M(GP_OP_ATAN, s)
 // every case whose destination slot is s (SS needs slot s + 1 as well)
 #define GP_SLOT_TU(s) GP_PUSH(s) GP_EACH_BIN(GP_BIN_T, s) GP_EACH_UN(GP_UN, s)
-#define GP_SLOT_B(s) GP_EACH_BIN(GP_BIN_SS, s)
+#define GP_SLOT_B(s) GP_EACH_BIN(GP_BIN_SS, s)   // SS and SSR
 
 #define GP_FOR_0_2(M) M(0) M(1) M(2)
 #define GP_FOR_0_6(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6)
@@ -185,10 +191,11 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
   const int n_groups = (count + a.G - 1) / a.G;
   const int64_t n_items = (int64_t)n_groups * a.n_chunks;
   double* acc = reinterpret_cast<double*>(smem);                 // [NW][G][S]
-  float* ys = reinterpret_cast<float*>(smem + (PREDICT ? 0 : smem_acc_bytes(a.G, S)));
-  float* ws = ys + TILE;
-  float* xs = ws + TILE;                                         // [n_cols][TILE] if XSMEM
   const bool has_w = a.w != nullptr;
+  float* ys = reinterpret_cast<float*>(smem + (PREDICT ? 0 : smem_acc_bytes(a.G, S)));
+  float* ws = ys + (PREDICT ? 0 : TILE);
+  float* xs = ws + (has_w ? TILE : 0);                           // [n_cols][TILE] if XSMEM
+  uint4* sw = reinterpret_cast<uint4*>(xs + (XSMEM ? a.n_cols * TILE : 0));  // stream window
   const float Ky = (!PREDICT && S == 3) ? *a.y_shift : 0.0f;
 
   // Persistent CTAs pull work items (program group g fastest, then row chunk q) from a queue;
@@ -218,7 +225,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
         const int64_t row = t0 + i;
         if constexpr (!PREDICT) {
           ys[i] = in ? a.y[row] : 0.0f;
-          ws[i] = in ? (has_w ? a.w[row] : 1.0f) : 0.0f;
+          if (has_w) ws[i] = in ? a.w[row] : 0.0f;
         }
         if constexpr (XSMEM) {
           for (int c = 0; c < a.n_cols; ++c)
@@ -228,7 +235,6 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
       __syncthreads();
 
       // ---- A3 + A4 + A5: walk the group's code stream --------------------------------------
-      const uint4* __restrict__ sp = a.stream + s_begin;
       int ebase = tid * 4;                           // element e(r) = ebase + (r/4)*NT*4 + r%4
       float l0 = 0.f, l1 = 0.f, l2 = 0.f;
       float st[STACK][R];
@@ -252,7 +258,13 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
 #pragma unroll
         for (int k = 0; k < R4; ++k) {
           const float4 yv = *reinterpret_cast<const float4*>(ys + ebase + k * NT * 4);
-          const float4 wv = *reinterpret_cast<const float4*>(ws + ebase + k * NT * 4);
+          float4 wv;
+          if (has_w) {
+            wv = *reinterpret_cast<const float4*>(ws + ebase + k * NT * 4);
+          } else {  // unweighted: w = 1 on rows of the tile, 0 on padding
+            const int e = ebase + k * NT * 4;
+            wv = make_float4(e < nvalid, e + 1 < nvalid, e + 2 < nvalid, e + 3 < nvalid);
+          }
           const float yy[4] = {yv.x, yv.y, yv.z, yv.w}, ww[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -298,36 +310,59 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
           }
         }
       };
-      // two-deep software prefetch of the (warp-uniform) stream words, uninterrupted across
-      // program boundaries
-      uint4 nxt = __ldg(sp), nxt2 = __ldg(sp + 1);
+      // The stream is read from a shared-memory window (copied by the whole CTA: once per item
+      // when the group's stream fits, else window by window per tile); each warp walks it with a
+      // two-deep prefetch that runs uninterrupted across program boundaries.
+      for (int64_t w0 = 0; w0 < s_len; w0 += kStreamWin) {
+        const int wn = (int)min((int64_t)kStreamWin, s_len - w0);
+        if (s_len > kStreamWin || t0 == r_begin) {
+          __syncthreads();                           // every warp is done with the old window
+          for (int i = tid; i < wn + 2; i += NT) sw[i] = __ldg(a.stream + s_begin + w0 + i);
+          __syncthreads();
+        }
+#if GP_PREFETCH_CASE_ONLY
+        // prefetch only the case ids (2 registers); the payload word is read from the window
+        // at the top of each iteration (its LDS latency overlaps the dispatch branch)
+        uint32_t c_n = sw[0].x, c_n2 = sw[1].x;
+#else
+        uint4 nxt = sw[0], nxt2 = sw[1];
+#endif
 #pragma unroll 1
-      for (int64_t kk = 0; kk < s_len; ++kk) {
-        const uint4 cw = nxt;
-        nxt = nxt2;
-        nxt2 = __ldg(sp + kk + 2);                   // stream buffer carries two pad words
-        switch (cw.x >> 2) {                         // .x = case id * 4 (jump-table offset)
-          GP_ALL_CASES
-          case kCaseEndPass: {                       // next row pass of the same program
-            end_pass(cw);
-            ebase = (int)cw.z * NT * R + tid * 4;
-          } break;
-          case kCaseEnd: {                           // program done: warp-reduce into smem (A5)
-            end_pass(cw);
-            if constexpr (!PREDICT) {
-              double* slot = acc + ((size_t)warp * a.G + cw.z) * S;
-              if (S == 1) {
-                const float v = warp_sum_f32(l0);
-                if (lane == 0) slot[0] += (double)v;
-              } else {
-                const double v0 = warp_sum_f64(l0), v1 = warp_sum_f64(l1), v2 = warp_sum_f64(l2);
-                if (lane == 0) { slot[0] += v0; slot[1] += v1; slot[2] += v2; }
+        for (int kk = 0; kk < wn; ++kk) {
+#if GP_PREFETCH_CASE_ONLY
+          const uint32_t cid = c_n;
+          c_n = c_n2;
+          c_n2 = sw[kk + 2].x;                       // window carries two look-ahead words
+          const uint4 cw = sw[kk];
+#else
+          const uint4 cw = nxt;
+          nxt = nxt2;
+          nxt2 = sw[kk + 2];                         // window carries two look-ahead words
+          const uint32_t cid = cw.x;
+#endif
+          switch (cid >> 2) {                        // case id * 4 (jump-table offset)
+            GP_ALL_CASES
+            case kCaseEndPass: {                     // next row pass of the same program
+              end_pass(cw);
+              ebase = (int)cw.z * NT * R + tid * 4;
+            } break;
+            case kCaseEnd: {                         // program done: warp-reduce into smem (A5)
+              end_pass(cw);
+              if constexpr (!PREDICT) {
+                double* slot = acc + ((size_t)warp * a.G + cw.z) * S;
+                if (S == 1) {
+                  const float v = warp_sum_f32(l0);
+                  if (lane == 0) slot[0] += (double)v;
+                } else {
+                  const double v0 = warp_sum_f64(l0), v1 = warp_sum_f64(l1), v2 = warp_sum_f64(l2);
+                  if (lane == 0) { slot[0] += v0; slot[1] += v1; slot[2] += v2; }
+                }
+                l0 = l1 = l2 = 0.f;
               }
-              l0 = l1 = l2 = 0.f;
-            }
-            ebase = tid * 4;
-          } break;
-          default: __builtin_unreachable();          // stage / pack guarantee a valid case
+              ebase = tid * 4;
+            } break;
+            default: __builtin_unreachable();        // stage / pack guarantee a valid case
+          }
         }
       }
     }

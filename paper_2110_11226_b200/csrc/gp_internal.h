@@ -25,7 +25,7 @@ struct EvalPlan {
 bool is_host_pointer(const void* p);
 int sm_count(int device);
 EvalPlan plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t n_cols, int S,
-                   bool predict);
+                   bool predict, bool weighted);
 
 }  // namespace gpb
 
@@ -35,7 +35,7 @@ struct gp_context {
   void* comm = nullptr;  // ncclComm_t
   std::string err;
   // device workspaces (grown on demand, stream-ordered)
-  gpb::StageBuf code, code_off, code_len, need, lists, pos, gstart, counts, codestream, status, partial,
+  gpb::StageBuf code, code_off, code_len, need, lists, pos, gstart, counts, codestream, scratch, status, partial,
       sums, shift, xref;
   // staging for [host] arguments
   gpb::StageBuf h_nodes, h_off, h_X, h_y, h_w, h_fit;
@@ -48,9 +48,10 @@ struct gp_context {
   double prof_ms = 0.0;
   int64_t prof_launches = 0;
   int64_t kernel_launches = 0;   // gp_context_kernel_launches
+  bool sethi_ullman = true;      // gp_context_set_eval_order
 
   std::vector<gpb::StageBuf*> all_buffers() {
-    return {&code, &code_off, &code_len, &need, &lists, &pos, &gstart, &counts, &codestream, &status,
+    return {&code, &code_off, &code_len, &need, &lists, &pos, &gstart, &counts, &codestream, &scratch, &status,
             &partial, &sums, &shift, &xref,
             &h_nodes, &h_off, &h_X, &h_y, &h_w, &h_fit};
   }

@@ -18,8 +18,10 @@ constexpr int kNumVariants = 4;
 constexpr int kVariantStack[kNumVariants] = {4, 8, 12, 20};
 
 // Stream marker cases (after every (op, variant, slot) case id).
-constexpr int kCaseEndPass = 116 * kCaseStride;   // OPV_COUNT * kCaseStride
+constexpr int kCaseEndPass = 123 * kCaseStride;   // OPV_COUNT * kCaseStride
 constexpr int kCaseEnd = kCaseEndPass + 1;
+// Code-stream window staged in shared memory per CTA (words of 16 B).
+constexpr int kStreamWin = 768;
 
 // Everything the fused evaluator needs for one launch (see eval_impl.cuh). Each variant runs a
 // packed CODE STREAM per program group: for every program of the group, SUB copies of its code

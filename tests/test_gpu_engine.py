@@ -93,3 +93,27 @@ def test_full_size_c3_sampled(gp, ctx, orc):
     sub_off[1:] = np.cumsum([lens[p] for p in sample])
     ref, sens, flags = orc.population_fitness(sub_nodes, sub_off, X, y, None, "mse")
     check_fitness(fit[sample], ref, sens, flags, "mse", max_excluded=1.0)
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_full_size_wide_configs_sampled(gp, ctx, orc, cfg):
+    """C4 (Higgs-shaped 11M x 28, log-loss, population 4096) and C5 (Year-shaped 1M x 90, RMSE,
+    depth 2-8) at full size through the engine (wide datasets -> global-X evaluator path); sampled
+    programs' fitness against the oracle over ALL rows."""
+    import bench
+    c = bench.CONFIGS[cfg]
+    X, y, _, _, m = bench.load_dataset(c)
+    e = gp.Engine(ctx, dev(X), dev(y), population_size=c["pop"], metric=c["metric"], seed=2110,
+                  init_depth_min=c["depth"][0], init_depth_max=c["depth"][1])
+    e.init_population()
+    e.generation()
+    nodes, off, fit = e.population()
+    lens = np.diff(off)
+    rng = np.random.default_rng(1)
+    sample = list(rng.choice(np.where(lens > 4)[0], 3, replace=False)) + [int(np.argmax(lens))]
+    sub_nodes = np.concatenate([nodes[off[p]:off[p + 1]] for p in sample])
+    sub_off = np.zeros(len(sample) + 1, np.int64)
+    sub_off[1:] = np.cumsum([lens[p] for p in sample])
+    ref, sens, flags = orc.population_fitness(sub_nodes, sub_off, X, y, None, c["metric"])
+    check_fitness(fit[sample], ref, sens, flags, c["metric"], max_excluded=1.0)
+    e.close()

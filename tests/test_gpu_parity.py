@@ -106,18 +106,48 @@ def test_predict_rows_match_oracle(gp, ctx, orc, funcs, max_stack, depth):
 
 
 @pytest.mark.parametrize("max_stack", [12, 20])
-def test_predict_every_stack_slot(gp, ctx, orc, max_stack):
-    """Left-deep programs whose stack need spans 1..max_stack exercise every (op, slot) case of
-    the 12- and 20-slot kernels; plus shallow random programs through the same kernel."""
+@pytest.mark.parametrize("sethi_ullman", [False, True])
+def test_predict_every_stack_slot(gp, ctx, orc, max_stack, sethi_ullman):
+    """Left-deep programs whose (reverse-prefix) stack need spans 1..max_stack exercise every
+    (op, slot) case of the 12- and 20-slot kernels in the classic order; with the Sethi-Ullman
+    order the same programs need few slots and exercise the reversed-operand (SSR) cases."""
     dn, do = synth.deep_population(60, seed=max_stack, need=(2, max_stack))
     rn, ro = synth.random_population(40, seed=3, depth=(1, 6), max_stack=8)
     nodes = np.concatenate([dn, rn])
     off = np.concatenate([do, ro[1:] + do[-1]])
     X, _ = synth.pagie_grid(40)
-    out, st = ctx.predict(dev(nodes), dev(off), dev(X), max_stack=max_stack)
+    ctx.set_eval_order(sethi_ullman)
+    try:
+        out, st = ctx.predict(dev(nodes), dev(off), dev(X), max_stack=max_stack)
+    finally:
+        ctx.set_eval_order(True)
     assert (st.cpu().numpy() == 0).all()
     checked, skipped = check_rows(orc, nodes, off, X, out.cpu().numpy())
     assert skipped <= 0.02 * (checked + skipped)
+
+
+def test_sethi_ullman_fits_balanced_need(gp, ctx, orc):
+    """chain_k = add(chain_{k-1}, sin(x)): both operands are computed values, so the classic
+    reverse-prefix order (sin(x) first) needs k slots while Sethi-Ullman (chain first) needs 2:
+    with max_stack = 4 the k = 6 chain is evaluated (and matches the oracle) only in
+    Sethi-Ullman order."""
+    x = ("var", 0)
+    toks = [x]
+    for _ in range(6):                       # chain_k = add(chain_{k-1}, sin(x))
+        toks = ["add"] + toks + ["sin", x]
+    chain = orc.program(*toks)
+    assert orc.validate(chain) == 0 and orc.stack_need(chain) >= 7
+    off = np.array([0, len(chain)], np.int64)
+    X, _ = synth.pagie_grid(16)
+    outs = {}
+    for su, ok in ((True, True), (False, False)):
+        ctx.set_eval_order(su)
+        outs[su], st = ctx.predict(dev(chain), dev(off), dev(X), max_stack=4)
+        assert (int(st.cpu()[0]) == 0) == ok
+    ctx.set_eval_order(True)
+    v, e, _ = orc.eval_program(chain, X)
+    g = outs[True].cpu().numpy()[0]
+    assert np.all(np.abs(g - v) <= np.maximum(1e-4 * np.abs(v), 4 * e + 1e-6))
 
 
 def test_predict_deep_random_all_ops_stress(gp, ctx, orc):
@@ -185,8 +215,12 @@ def test_evaluate_fitness_matches_oracle(gp, ctx, orc, metric, weighted):
 def test_evaluate_deep_variants(gp, ctx, orc, max_stack, metric):
     X, y = synth.pagie_grid(40)
     nodes, off = synth.deep_population(80, seed=max_stack, need=(2, max_stack))
-    fit, st = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric=metric,
-                           max_stack=max_stack)
+    ctx.set_eval_order(False)                # classic order: the deep slots of the 12/20 kernels
+    try:
+        fit, st = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric=metric,
+                               max_stack=max_stack)
+    finally:
+        ctx.set_eval_order(True)
     ref, sens, flags = orc.population_fitness(nodes, off, X, y, None, metric)
     check_fitness(fit.cpu().numpy(), ref, sens, flags, metric)
 
