@@ -44,7 +44,9 @@ CONFIGS = {
                data="year", rows=1_048_576, pop=8192, metric="rmse", depth=(2, 8)),
 }
 # Algorithmic SFU (MUFU) operations per node-row: the transcendental /
-# reciprocal evaluations the method itself requires, whatever the implementation.
+# reciprocal evaluations the method itself requires, whatever the implementation. Counted only
+# for nodes whose subtree depends on a variable (stats op_count); variable-free subtrees are
+# per-program constants, not per-row work.
 SFU_COST = {5: 1, 9: 1, 10: 1, 11: 3, 14: 1, 15: 1, 16: 1, 17: 1, 8: 2, 20: 2, 21: 2, 22: 2,
             23: 1, 24: 1, 25: 1}
 FP32_COST = {2: 1, 3: 1, 4: 1, 5: 1, 6: 1, 7: 1, 9: 1, 10: 1, 11: 2, 12: 1, 13: 1, 18: 1, 19: 2}
@@ -122,6 +124,24 @@ def algorithmic_ops(op_count, rows, metric, n_programs):
     return sfu, fp32
 
 
+def roofline_of(sfu, fp32, eval_ms, launches, step_ms):
+    """Binding ALU pipe of the evaluator for the given algorithmic work: SFU (MUFU) or FP32."""
+    eval_s = eval_ms * 1e-3
+    f_sfu, f_fp32 = sfu / eval_s / SFU_PEAK, fp32 / eval_s / FP32_PEAK
+    if f_sfu >= f_fp32:
+        r = {"bound": "alu", "pipe": "SFU (MUFU)", "achieved": round(sfu / eval_s / 1e12, 4),
+             "peak": round(SFU_PEAK / 1e12, 4), "unit": "Tops/s (MUFU)", "frac": round(f_sfu, 4)}
+    else:
+        r = {"bound": "alu", "pipe": "FP32", "achieved": round(fp32 / eval_s / 1e12, 4),
+             "peak": round(FP32_PEAK / 1e12, 4), "unit": "TFLOP/s (fp32)", "frac": round(f_fp32, 4)}
+    r.update({"traffic": ncu_traffic(), "sfu_frac": round(f_sfu, 4), "fp32_frac": round(f_fp32, 4),
+              "eval_ms_per_launch": round(eval_ms / max(launches, 1), 3),
+              "eval_share_of_step": round(eval_ms / step_ms, 4),
+              "peak_note": "SFU: 148 SMs x 16 MUFU/clk x 1965 MHz (measured MUFU.SIN 4.63e12/s); "
+                           "FP32: 148 x 128 x 1965 MHz"})
+    return r
+
+
 def ncu_traffic():
     """dram bytes per eval launch from the committed ncu --set full summary, if present."""
     path = os.path.join(ROOT, "profiles", "eval_kernel_ncu.json")
@@ -182,7 +202,9 @@ def run_b200(args, cfg):
     kw = dict(population_size=cfg["pop"], metric=cfg["metric"], seed=2110,
               init_depth_min=cfg["depth"][0], init_depth_max=cfg["depth"][1])
     eng = gp.Engine(ctx, X, y, **kw)
-    eng.init_population()
+    st0 = eng.init_population()
+    n0, o0, _ = eng.population()
+    gen0 = (n0, o0, st0["op_count"])
     for _ in range(args.warmup):
         eng.generation()
 
@@ -216,21 +238,40 @@ def run_b200(args, cfg):
     ms, eval_ms_max = float(t[0]), float(t[1])
     value = node_evals / (ms * 1e-3)
 
-    # roofline of the dominant kernel (the fused evaluator), this rank's launches
+    # roofline of the dominant kernel (the fused evaluator), this rank's launches: algorithmic
+    # per-row work = variable-dependent nodes only (variable-free subtrees are constants)
     rows_local = X.shape[1]
     sfu = fp32 = 0
     for s in steps:
-        a, b = algorithmic_ops(s["op_count"], rows_local, cfg["metric"], cfg["pop"])
-        sfu, fp32 = sfu + a, fp32 + b
-    eval_s = eval_ms * 1e-3
-    achieved = sfu / eval_s / 1e12
-    roofline = {"bound": "alu", "pipe": "SFU (MUFU)", "achieved": round(achieved, 4),
-                "peak": round(SFU_PEAK / 1e12, 4), "unit": "Tops/s (MUFU)",
-                "frac": round(achieved / (SFU_PEAK / 1e12), 4), "traffic": ncu_traffic(),
-                "fp32_frac": round(fp32 / eval_s / FP32_PEAK, 4),
-                "eval_ms_per_launch": round(eval_ms / max(eval_launches, 1), 3),
-                "eval_share_of_step": round(eval_ms / ms, 4),
-                "peak_note": "148 SMs x 16 MUFU/clk x 1965 MHz; measured MUFU.SIN 4.63e12/s"}
+        a, b2 = algorithmic_ops(s["op_count"], rows_local, cfg["metric"], cfg["pop"])
+        sfu, fp32 = sfu + a, fp32 + b2
+    roofline = roofline_of(sfu, fp32, eval_ms, eval_launches, ms)
+    var_nodes = sum(sum(s["op_count"]) for s in steps) * m_global
+    const_share = float(np.mean([s["const_nodes"] / max(1, s["total_nodes"]) for s in steps]))
+
+    # the same kernel on the generation-0 (ramped half-and-half) population, which carries far
+    # more per-row transcendental work than evolved populations: a capability point
+    roof0 = None
+    if gen0 is not None:
+        n0, o0, ops0 = gen0
+        nd, of = torch.from_numpy(n0).cuda(local), torch.from_numpy(o0).cuda(local)
+        fit_buf = torch.empty(len(o0) - 1, dtype=torch.float32, device=f"cuda:{local}")
+        for _ in range(2):
+            ctx.evaluate(nd, of, X, y, metric=cfg["metric"], max_stack=20, fitness_out=fit_buf)
+        torch.cuda.synchronize()
+        ctx.set_profiling(True)
+        ctx.eval_timing(reset=True)
+        reps = 5
+        for _ in range(reps):
+            ctx.evaluate(nd, of, X, y, metric=cfg["metric"], max_stack=20, fitness_out=fit_buf)
+        torch.cuda.synchronize()
+        ms0, l0 = ctx.eval_timing(reset=True)
+        ctx.set_profiling(False)
+        a0, b0 = algorithmic_ops(ops0, rows_local, cfg["metric"], cfg["pop"])
+        roof0 = roofline_of(a0 * reps, b0 * reps, ms0, l0, ms0)
+        roof0["node_evals_per_s"] = float(len(n0)) * rows_local * reps / (ms0 * 1e-3)
+        roof0["population"] = "generation 0 (ramped half-and-half), mean length %.2f" % (
+            len(n0) / (len(o0) - 1))
 
     # ---- end-to-end: dataset streamed from pinned host memory every step ------------------------
     e2e = None
@@ -278,7 +319,9 @@ def run_b200(args, cfg):
                        "metric": cfg["metric"], "mean_program_length": round(mean_len, 3),
                        "parallelism": f"rows sharded over {world} GPU(s)",
                        "l2": "inputs larger than L2 (X + y = %.0f MB)" % ((Xh.nbytes + yh.nbytes) * world / 1e6)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "roofline_gen0": roof0,
+            "var_node_evals_per_s": var_nodes / (ms * 1e-3), "const_node_share": round(const_share, 4),
+            "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "phases_ms_per_step": {k: round(1e3 * float(np.mean([s[k] for s in steps])), 3)

@@ -241,7 +241,9 @@ typedef struct {
   int32_t max_stack_need;
   int32_t n_tournaments;
   double t_select_s, t_mutate_s, t_h2d_s, t_eval_s, t_total_s; /* phase wall times */
-  int64_t op_count[GP_OP_COUNT]; /* histogram of opcodes in the evaluated population */
+  int64_t op_count[GP_OP_COUNT]; /* opcode histogram of the evaluated population's nodes whose
+                                   subtree contains a variable (per-row work) */
+  int64_t const_nodes;           /* nodes of variable-free subtrees (per-program constants) */
 } gp_generation_stats;
 
 /* Creates an engine over a dataset. X / y / w are [host|device] (same layouts as gp_evaluate);

@@ -63,7 +63,7 @@ class GpGenerationStats(ctypes.Structure):
         ("best_len", i32), ("best_depth", i32), ("mean_raw", f64), ("total_nodes", i64),
         ("max_stack_need", i32), ("n_tournaments", i32), ("t_select_s", f64),
         ("t_mutate_s", f64), ("t_h2d_s", f64), ("t_eval_s", f64), ("t_total_s", f64),
-        ("op_count", i64 * 26),
+        ("op_count", i64 * 26), ("const_nodes", i64),
     ]
 
     def as_dict(self):

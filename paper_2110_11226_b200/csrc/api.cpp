@@ -350,7 +350,7 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   // stream words <= SUB_max x (code words + one marker per program) + 2 pad words
   if ((s = ctx->grow(&ctx->codestream.p, &ctx->codestream.cap, ((size_t)4 * (n_nodes + n) + 2) * sizeof(uint4), "stream"))) return s;
   if ((s = ctx->grow(&ctx->status.p, &ctx->status.cap, (size_t)n * sizeof(uint32_t), "status"))) return s;
-  if ((s = ctx->grow(&ctx->scratch.p, &ctx->scratch.cap, (size_t)2 * n_nodes * sizeof(int32_t), "scratch"))) return s;
+  if ((s = ctx->grow(&ctx->scratch.p, &ctx->scratch.cap, (size_t)4 * n_nodes * sizeof(int32_t), "scratch"))) return s;
   if ((s = ctx->launch(launch_stage(programs, offsets, n_programs, n_nodes, n_cols, max_stack,
                                   (uint4*)ctx->code.p, (int64_t*)ctx->code_off.p,
                                   (int32_t*)ctx->code_len.p, (int32_t*)ctx->need.p,

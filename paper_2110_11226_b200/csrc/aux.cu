@@ -13,8 +13,9 @@ namespace gpb {
 // ---------------------------------------------------------------------------------------------
 // Stage / compile. One thread per program (programs are short; a few µs total).
 //  - prefix validation with the needed-counter scan, opcode and variable-range checks
-//  - a bottom-up pass computes every subtree's stack need with terminals folded into their
-//    parent's code word and the Sethi-Ullman order (evaluate the child needing more slots first;
+//  - a bottom-up pass folds variable-free subtrees into constants (evaluated once, with the
+//    evaluator's fp32 op functions) and computes every subtree's stack need with terminals folded
+//    into their parent's code word and the Sethi-Ullman order (evaluate the child needing more slots first;
 //    the classic reverse-prefix order of P:194 is the default, swapped only when it needs more);
 //    a post-order emission then writes one code word per function node with its static
 //    destination slot (device_ops.cuh "compiled program code"); stack need > capacity ->
@@ -49,44 +50,75 @@ __global__ void stage_kernel(const gp_node* __restrict__ nodes, const int64_t* _
   int64_t emitted = 0;
   int need_root = 0;
   if (!flags) {
-    // (1) bottom-up (reverse prefix) pass: subtree end and stack need of every node, with
-    // terminals folded into their parents (need 0) and Sethi-Ullman child order for binary nodes
-    // whose operands are both stack values: evaluate the child needing more slots first.
+    // (1) bottom-up (reverse prefix) pass over the nodes: subtree end, constant folding and stack
+    // need. A variable-free subtree is evaluated ONCE here, with the same fp32 op functions the
+    // evaluator uses, and becomes a constant operand of its parent (per-program constant, not
+    // per-row work). Terminal and constant operands are folded into their parent's code word
+    // (need 0); binary nodes whose operands are both computed values use the Sethi-Ullman order
+    // (evaluate the child needing more slots first) unless the classic order is requested.
     int32_t* nd_need = scratch + b;               // per node
     int32_t* nd_end = scratch + n_nodes + b;      // per node (relative to b)
+    int32_t* nd_cst = scratch + 2 * n_nodes + b;  // 1: variable-free subtree
+    uint32_t* nd_val = reinterpret_cast<uint32_t*>(scratch + 3 * n_nodes + b);  // its fp32 value
     const int64_t len = e - b;
     for (int64_t i = len - 1; i >= 0; --i) {
-      const int a = op_arity(nodes[b + i].op);
-      if (a == 0) { nd_need[i] = 0; nd_end[i] = (int32_t)(i + 1); continue; }
+      const gp_node nd = nodes[b + i];
+      const int a = op_arity(nd.op);
+      if (a == 0) {
+        nd_need[i] = 0;
+        nd_end[i] = (int32_t)(i + 1);
+        nd_cst[i] = nd.op == GP_OP_CONST;
+        nd_val[i] = __float_as_uint(nd.value);
+        continue;
+      }
       const int64_t A = i + 1;
-      const int nA = nd_need[A];
-      if (a == 1) { nd_need[i] = nA > 0 ? nA : 1; nd_end[i] = nd_end[A]; continue; }
+      if (a == 1) {
+        nd_end[i] = nd_end[A];
+        nd_cst[i] = nd_cst[A];
+        if (nd_cst[A]) {
+          nd_val[i] = __float_as_uint(apply_rt(nd.op, __uint_as_float(nd_val[A]), 0.0f));
+          nd_need[i] = 0;
+        } else {
+          nd_need[i] = nd_need[A] > 0 ? nd_need[A] : 1;
+        }
+        continue;
+      }
       const int64_t B = nd_end[A];
-      const int nB = nd_need[B];
+      nd_end[i] = nd_end[B];
+      nd_cst[i] = nd_cst[A] && nd_cst[B];
+      if (nd_cst[i]) {
+        nd_val[i] = __float_as_uint(apply_rt(nd.op, __uint_as_float(nd_val[A]),
+                                             __uint_as_float(nd_val[B])));
+        nd_need[i] = 0;
+        continue;
+      }
+      const int nA = nd_need[A], nB = nd_need[B];
       int n;
       if (nA == 0 || nB == 0) n = max(max(nA, nB), 1);
       else n = sethi_ullman ? min(max(nB, 1 + nA), max(nA, 1 + nB)) : max(nB, 1 + nA);
       nd_need[i] = n;
-      nd_end[i] = nd_end[B];
     }
-    need_root = len == 1 ? 1 : nd_need[0];
+    need_root = (len == 1 || nd_cst[0]) ? 1 : nd_need[0];
     if (need_root > cap) flags |= GP_FLAG_STACK_OVERFLOW;
   }
   if (!flags) {
-    // (2) post-order emission with the chosen child order; terminal operands go into the word
+    // (2) post-order emission with the chosen child order; terminal and folded-constant operands
+    // go into the parent's word
     const int32_t* nd_need = scratch + b;
     const int32_t* nd_end = scratch + n_nodes + b;
+    const int32_t* nd_cst = scratch + 2 * n_nodes + b;
+    const uint32_t* nd_val = reinterpret_cast<const uint32_t*>(scratch + 3 * n_nodes + b);
     auto src = [&](int64_t i, uint32_t* pl) -> int {  // 0 stack, 1 variable, 2 constant
       const gp_node nd = nodes[b + i];
       if (nd.op == GP_OP_VAR) { *pl = (uint32_t)nd.var; return 1; }
-      if (nd.op == GP_OP_CONST) { *pl = __float_as_uint(nd.value); return 2; }
+      if (nd_cst[i]) { *pl = nd_val[i]; return 2; }
       *pl = 0u;
       return 0;
     };
     auto emit = [&](int opv, int slot, uint32_t pa, uint32_t pb) {
       code[b + emitted++] = make_uint4((uint32_t)(opv * kCaseStride + slot) * 4u, pa, pb, 0u);
     };
-    if (e - b == 1) {
+    if (e - b == 1 || nd_cst[0]) {
       uint32_t pl;
       const int k = src(0, &pl);
       emit(k == 1 ? OPV_PUSH_V : OPV_PUSH_C, 0, pl, 0u);

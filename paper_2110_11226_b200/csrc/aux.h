@@ -10,7 +10,7 @@ namespace gpb {
 cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n_programs,
                          int64_t n_nodes, int32_t n_cols, int32_t max_stack, uint4* code,
                          int64_t* code_off, int32_t* code_len, int32_t* need, uint32_t* status,
-                         int32_t* scratch /* 2 x n_nodes int32 */, int32_t sethi_ullman,
+                         int32_t* scratch /* 4 x n_nodes int32 */, int32_t sethi_ullman,
                          cudaStream_t s);
 // Partitions valid programs by stack need into kNumVariants ascending lists, lays out each
 // variant's code stream (per-program offsets, group starts for G programs per group), zeroes the

@@ -235,6 +235,7 @@ struct gp_engine {
   int generation = -1;
   int max_need = 1;
   int64_t op_count[GP_OP_COUNT] = {};
+  int64_t const_nodes = 0;
   // flat CSR (pinned host) and its device copy
   gp_node* h_nodes = nullptr;
   int64_t* h_off = nullptr;
@@ -324,10 +325,28 @@ struct gp_engine {
     });
     max_need = 1;
     for (int v : needs) max_need = std::max(max_need, v);
+    // opcode histogram of variable-dependent nodes (per-row work); variable-free subtrees are
+    // per-program constants and are counted separately
     std::fill(op_count, op_count + GP_OP_COUNT, (int64_t)0);
-    for (int64_t i = 0; i < total; ++i) {
-      const int op = h_nodes[i].op;
-      if (op >= 0 && op < GP_OP_COUNT) ++op_count[op];
+    const_nodes = 0;
+    std::vector<char> is_const;
+    for (int p = 0; p < n; ++p) {
+      const Prog& pr = pop[p];
+      is_const.assign(pr.size(), 0);
+      std::vector<int64_t> kids;  // reverse-prefix stack of child indices
+      for (int64_t i = (int64_t)pr.size() - 1; i >= 0; --i) {
+        const int op = pr[i].op;
+        const int ar = arity(op);
+        bool c = op == GP_OP_CONST;
+        if (ar > 0) {
+          c = true;
+          for (int k = 0; k < ar; ++k) { c = c && is_const[kids.back()]; kids.pop_back(); }
+        }
+        is_const[i] = c;
+        kids.push_back(i);
+        if (c) ++const_nodes;
+        else if (op >= 0 && op < GP_OP_COUNT) ++op_count[op];
+      }
     }
     n_nodes = total;
     gp_status s;
@@ -370,6 +389,7 @@ struct gp_engine {
     st->total_nodes = n_nodes;
     st->max_stack_need = max_need;
     std::copy(op_count, op_count + GP_OP_COUNT, st->op_count);
+    st->const_nodes = const_nodes;
     if (best >= 0) {
       const float pen = cfg.parsimony * (float)pop[best].size();
       st->best_raw = fit[best];
