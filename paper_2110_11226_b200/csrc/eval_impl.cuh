@@ -179,6 +179,22 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
   return v;
 }
 
+// Transposed butterfly: the warp sums of four per-lane values with 6 shuffles (instead of 4 x 5):
+// afterwards lane 0 holds sum(v0), lane 8 sum(v1), lane 16 sum(v2), lane 24 sum(v3).
+__device__ __forceinline__ float warp_sum4_f32(float v0, float v1, float v2, float v3, int lane) {
+  const bool lo16 = (lane & 16) == 0, lo8 = (lane & 8) == 0;
+  float k0 = lo16 ? v0 : v2, k1 = lo16 ? v1 : v3;
+  const float s0 = lo16 ? v2 : v0, s1 = lo16 ? v3 : v1;
+  k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+  float m = lo8 ? k0 : k1;
+  m += __shfl_xor_sync(0xffffffffu, lo8 ? k1 : k0, 8);
+  m += __shfl_xor_sync(0xffffffffu, m, 4);
+  m += __shfl_xor_sync(0xffffffffu, m, 2);
+  m += __shfl_xor_sync(0xffffffffu, m, 1);
+  return m;
+}
+
 template <bool PREDICT, bool XSMEM>
 // the global-X instantiation holds more live addresses: one resident CTA less
 __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB - 1 : 1))
@@ -237,6 +253,18 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
       // ---- A3 + A4 + A5: walk the group's code stream --------------------------------------
       int ebase = tid * 4;                           // element e(r) = ebase + (r/4)*NT*4 + r%4
       float l0 = 0.f, l1 = 0.f, l2 = 0.f;
+      // single-sum metrics: per-lane sums of up to three finished programs wait here so four
+      // programs share one transposed warp reduction (warp_sum4_f32)
+      float pend0 = 0.f, pend1 = 0.f, pend2 = 0.f;
+      int pidx0 = 0, pidx1 = 0, pidx2 = 0, npend = 0;
+      auto reduce4 = [&](float v3, int i3, int n) {   // n programs valid (1..4)
+        const float m = warp_sum4_f32(pend0, pend1, pend2, v3, lane);
+        const int j = lane >> 3;
+        if ((lane & 7) == 0 && j < n) {
+          const int pl = j == 0 ? pidx0 : j == 1 ? pidx1 : j == 2 ? pidx2 : i3;
+          acc[(size_t)warp * a.G + pl] += (double)m;
+        }
+      };
       float st[STACK][R];
       // fused weighted loss of the current pass's rows (A4)
       auto loss = [&](auto tag, float Kp) {
@@ -351,8 +379,14 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
               if constexpr (!PREDICT) {
                 double* slot = acc + ((size_t)warp * a.G + cw.z) * S;
                 if (S == 1) {
-                  const float v = warp_sum_f32(l0);
-                  if (lane == 0) slot[0] += (double)v;
+                  if (npend == 3) {                  // fourth program: one batched reduction
+                    reduce4(l0, (int)cw.z, 4);
+                    npend = 0;
+                  } else {
+                    pend0 = pend1; pend1 = pend2; pend2 = l0;
+                    pidx0 = pidx1; pidx1 = pidx2; pidx2 = (int)cw.z;
+                    ++npend;
+                  }
                 } else {
                   const double v0 = warp_sum_f64(l0), v1 = warp_sum_f64(l1), v2 = warp_sum_f64(l2);
                   if (lane == 0) { slot[0] += v0; slot[1] += v1; slot[2] += v2; }
@@ -364,6 +398,14 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
             default: __builtin_unreachable();        // stage / pack guarantee a valid case
           }
         }
+      }
+      if (!PREDICT && S == 1 && npend > 0) {         // leftover batch at the end of the tile
+        // pending programs sit in the LAST npend slots of (pend0, pend1, pend2)
+        const int n = npend;
+        if (n == 1) { pend0 = pend2; pidx0 = pidx2; pend1 = pend2 = 0.f; }
+        else if (n == 2) { pend0 = pend1; pidx0 = pidx1; pend1 = pend2; pidx1 = pidx2; pend2 = 0.f; }
+        reduce4(0.f, 0, n);
+        npend = 0;
       }
     }
 
