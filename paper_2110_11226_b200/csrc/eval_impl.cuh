@@ -82,10 +82,14 @@ __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
   } else {                                                                                     \
     const float* xv_ = a.X + (int64_t)(var) * a.ldx + t0;                                      \
     const int e_ = ebase + (k) * NT * 4;                                                       \
-    v.x = __ldg(xv_ + min(e_, nvalid - 1));                                                    \
-    v.y = __ldg(xv_ + min(e_ + 1, nvalid - 1));                                                \
-    v.z = __ldg(xv_ + min(e_ + 2, nvalid - 1));                                                \
-    v.w = __ldg(xv_ + min(e_ + 3, nvalid - 1));                                                \
+    if (x_vec && nvalid == TILE) {                   /* full, 16-byte aligned tile: LDG.128 */ \
+      v = __ldg(reinterpret_cast<const float4*>(xv_ + e_));                                    \
+    } else {                                                                                   \
+      v.x = __ldg(xv_ + min(e_, nvalid - 1));                                                  \
+      v.y = __ldg(xv_ + min(e_ + 1, nvalid - 1));                                              \
+      v.z = __ldg(xv_ + min(e_ + 2, nvalid - 1));                                              \
+      v.w = __ldg(xv_ + min(e_ + 3, nvalid - 1));                                              \
+    }                                                                                          \
   }
 #define GP_CONST(w) __uint_as_float(w)
 #define GP_ROWS(stmt) _Pragma("unroll") for (int r = 0; r < R; ++r) { stmt; }
@@ -208,6 +212,8 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
   const int64_t n_items = (int64_t)n_groups * a.n_chunks;
   double* acc = reinterpret_cast<double*>(smem);                 // [NW][G][S]
   const bool has_w = a.w != nullptr;
+  // global-X path: 16-byte vector loads when every column start is 16-byte aligned
+  const bool x_vec = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && ((a.ldx & 3) == 0);
   float* ys = reinterpret_cast<float*>(smem + (PREDICT ? 0 : smem_acc_bytes(a.G, S)));
   float* ws = ys + (PREDICT ? 0 : TILE);
   float* xs = ws + (has_w ? TILE : 0);                           // [n_cols][TILE] if XSMEM

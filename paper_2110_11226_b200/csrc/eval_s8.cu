@@ -3,5 +3,5 @@
 #define GP_R 8
 #define GP_SUB 2
 #define GP_NT 128
-#define GP_MINB 5
+#define GP_MINB 4
 #include "eval_impl.cuh"
