@@ -347,7 +347,7 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   if ((s = ctx->grow(&ctx->pos.p, &ctx->pos.cap, (size_t)n * kNumVariants * sizeof(int64_t), "pos"))) return s;
   if ((s = ctx->grow(&ctx->gstart.p, &ctx->gstart.cap, (size_t)(n + 1) * kNumVariants * sizeof(int64_t), "gstart"))) return s;
   if ((s = ctx->grow(&ctx->counts.p, &ctx->counts.cap, 2 * kNumVariants * sizeof(int32_t) + (kNumVariants + 1) * sizeof(int64_t), "counts"))) return s;
-  // stream words <= SUB_max x (code words + one marker per program) + 2 pad words
+  // stream words <= SUB_max x code words + 2 pad words
   if ((s = ctx->grow(&ctx->codestream.p, &ctx->codestream.cap, ((size_t)4 * (n_nodes + n) + 2) * sizeof(uint4), "stream"))) return s;
   if ((s = ctx->grow(&ctx->status.p, &ctx->status.cap, (size_t)n * sizeof(uint32_t), "status"))) return s;
   if ((s = ctx->grow(&ctx->scratch.p, &ctx->scratch.cap, (size_t)4 * n_nodes * sizeof(int32_t), "scratch"))) return s;
@@ -388,8 +388,8 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
                      "bucket kernel"))) return s;
   return ctx->launch(launch_pack((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
                                (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->lists.p,
-                               (const int64_t*)ctx->pos.p, counts, base, shift, n_programs, G,
-                               subs, (uint4*)ctx->codestream.p, ctx->stream),
+                               (const int64_t*)ctx->pos.p, counts, base, n_programs, G, subs,
+                               (uint4*)ctx->codestream.p, ctx->stream),
                    "pack kernel");
 }
 
@@ -437,6 +437,7 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
   a.n_chunks = pl.n_chunks;
   a.partial = (double*)ctx->partial.p;
   a.ld_part = ld_part;
+  a.shift = metric == GP_PEARSON ? (const float*)ctx->shift.p : nullptr;
   a.y_shift = metric == GP_PEARSON ? (const float*)ctx->shift.p + n_programs : nullptr;
   ctx->last_plan = pl;
   if ((s = ctx->launch(launch_consts(y, w, n_rows, pl.rows_per_chunk, pl.n_chunks, a.y_shift,

@@ -200,7 +200,7 @@ cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n
 // ---------------------------------------------------------------------------------------------
 // Bucketing by stack need + code-stream layout (one CTA of 1024 threads). Program p goes to the
 // first variant whose register stack holds its need; each bucket list keeps ascending program
-// order (deterministic). Each variant's stream holds, per program, SUB_b x (code words + 1 marker);
+// order (deterministic). Each variant's stream holds, per program, SUB_b copies of its code words;
 // pos / gstart are absolute stream offsets (group g of bucket b starts at gstart[b][g]).
 // ---------------------------------------------------------------------------------------------
 namespace {
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
     if (tid == 0) base[b] = running;
     for (int c0 = 0; c0 < cb; c0 += 1024) {
       const int j = c0 + tid;
-      const int64_t words = j < cb ? (int64_t)subs[b] * (code_len[lists[(int64_t)b * n + j]] + 1) : 0;
+      const int64_t words = j < cb ? (int64_t)subs[b] * code_len[lists[(int64_t)b * n + j]] : 0;
       int64_t ex;
       const int64_t tot = block_exclusive_scan(words, &ex, warp_tot);
       if (j < cb) {
@@ -306,13 +306,14 @@ cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t 
   return cudaGetLastError();
 }
 
-// One thread per (bucket, list entry): SUB copies of the program's code, each followed by a
-// marker word: END_PASS {case, p, next pass, K_p bits} or END {case, p, index in group, K_p bits}.
+// One thread per (bucket, list entry): SUB copies of the program's code, one per row pass. The
+// last word of each pass carries the pass flags in .w (kernels.h kEndPass / kEndProgram): the next
+// pass index, or the program's slot in its group at the end of the last pass.
 __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __restrict__ code_off,
                             const int32_t* __restrict__ code_len, const int32_t* __restrict__ lists,
                             const int64_t* __restrict__ pos, const int32_t* __restrict__ counts,
-                            const int64_t* __restrict__ base, const float* __restrict__ shift,
-                            int32_t n, int32_t G, int4 sub4, uint4* __restrict__ stream) {
+                            const int64_t* __restrict__ base, int32_t n, int32_t G, int4 sub4,
+                            uint4* __restrict__ stream) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) stream[base[kNumVariants]] = stream[base[kNumVariants] + 1] = make_uint4(0, 0, 0, 0);
   if (i >= (int64_t)kNumVariants * n) return;
@@ -322,24 +323,23 @@ __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __res
   const int p = lists[i];
   const int len = code_len[p];
   const uint4* src = code + code_off[p];
-  const uint32_t kp = shift ? __float_as_uint(shift[p]) : 0u;
   uint4* dst = stream + pos[i];
   for (int pass = 0; pass < subs[b]; ++pass) {
     for (int k = 0; k < len; ++k) *dst++ = src[k];
     const bool last = pass == subs[b] - 1;
-    *dst++ = last ? make_uint4((uint32_t)kCaseEnd * 4u, (uint32_t)p, (uint32_t)(j % G), kp)
-                  : make_uint4((uint32_t)kCaseEndPass * 4u, (uint32_t)p, (uint32_t)(pass + 1), kp);
+    dst[-1].w = last ? (kEndProgram | ((uint32_t)(j % G) << 8))
+                     : (kEndPass | ((uint32_t)(pass + 1) << 8));
   }
 }
 
 cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                         const int32_t* lists, const int64_t* pos, const int32_t* counts,
-                        const int64_t* base, const float* shift, int32_t n_programs, int32_t G,
-                        const int* subs, uint4* stream, cudaStream_t s) {
+                        const int64_t* base, int32_t n_programs, int32_t G, const int* subs,
+                        uint4* stream, cudaStream_t s) {
   const int nt = 256;
   const int64_t total = (int64_t)kNumVariants * n_programs;
   pack_kernel<<<(unsigned)((total + nt - 1) / nt), nt, 0, s>>>(code, code_off, code_len, lists,
-                                                               pos, counts, base, shift,
+                                                               pos, counts, base,
                                                                n_programs, G,
                                                                make_int4(subs[0], subs[1], subs[2],
                                                                          subs[3]),

@@ -19,11 +19,11 @@ cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n
 cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
                           int32_t G, const int* subs, int32_t* lists, int64_t* pos,
                           int64_t* gstart, int32_t* counts, int64_t* base, cudaStream_t s);
-// Copies every bucketed program's code into its variant stream with the pass / end markers.
+// Copies every bucketed program's code into its variant stream, flagging the end of each pass.
 cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                         const int32_t* lists, const int64_t* pos, const int32_t* counts,
-                        const int64_t* base, const float* shift, int32_t n_programs, int32_t G,
-                        const int* subs, uint4* stream, cudaStream_t s);
+                        const int64_t* base, int32_t n_programs, int32_t G, const int* subs,
+                        uint4* stream, cudaStream_t s);
 // Dataset constants W, S_y, S_yy per row chunk -> partial[q][col0 .. col0 + 2].
 cudaError_t launch_consts(const float* y, const float* w, int64_t n_rows, int64_t rows_per_chunk,
                           int64_t n_chunks, const float* y_shift, double* partial, int64_t ld_part,

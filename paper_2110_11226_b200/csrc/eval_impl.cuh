@@ -10,8 +10,8 @@
 //     stage y, w (and X when n_cols is small) into shared memory, coalesced, zero-padded  [A2]
 //     walk the group's packed code stream (aux.cu pack_kernel): for each program of the group
 //     (programs of this variant's stack-need bucket), SUB copies of its code, one per row pass,
-//     each closed by a marker word whose case does the loss / reduction -- one contiguous stream,
-//     so the 2-deep code prefetch never restarts at a program boundary:
+//     the last word of each pass flagged so the loss / reduction follows its case -- one
+//     contiguous stream, so the 2-deep code prefetch never restarts at a program boundary:
 //       -- warp-uniform control flow: all lanes run the same program, no divergence
 //       for each of SUB passes: run the compiled code on R rows per thread with the stack in
 //         REGISTERS: the destination slot of every code word is static (stage kernel) and terminal
@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
     const int g = (int)(item % n_groups);
     const int64_t q = item / n_groups;
     const int np = min(a.G, count - g * a.G);
+    const int32_t* __restrict__ gids = a.prog_ids + (int64_t)g * a.G;   // group's program ids
     const int64_t s_begin = a.gstart[g], s_len = a.gstart[g + 1] - s_begin;
     if constexpr (!PREDICT) {
       for (int i = tid; i < NW * a.G * S; i += NT) acc[i] = 0.0;
@@ -325,22 +326,22 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
           }
         }
       };
-      // end of one row pass of program p: prediction store or loss
-      auto end_pass = [&](const uint4& cw) {
+      // end of one row pass of the program in group slot `pslot`: prediction store or loss
+      int pslot = 0;
+      auto end_pass = [&]() {
         if constexpr (PREDICT) {
-          float* o = a.out + (int64_t)cw.y * a.ld_out + t0;
+          float* o = a.out + (int64_t)gids[pslot] * a.ld_out + t0;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const int e = ebase + (r >> 2) * NT * 4 + (r & 3);
             if (e < nvalid) o[e] = st[0][r];
           }
         } else {
-          const float Kp = __uint_as_float(cw.w);
           switch (a.metric) {
-            case GP_MAE: loss(MTag<GP_MAE>{}, Kp); break;
-            case GP_MSE: case GP_RMSE: loss(MTag<GP_MSE>{}, Kp); break;
-            case GP_LOGLOSS: loss(MTag<GP_LOGLOSS>{}, Kp); break;
-            default: loss(MTag<GP_PEARSON>{}, Kp); break;
+            case GP_MAE: loss(MTag<GP_MAE>{}, 0.0f); break;
+            case GP_MSE: case GP_RMSE: loss(MTag<GP_MSE>{}, 0.0f); break;
+            case GP_LOGLOSS: loss(MTag<GP_LOGLOSS>{}, 0.0f); break;
+            default: loss(MTag<GP_PEARSON>{}, __ldg(a.shift + gids[pslot])); break;
           }
         }
       };
@@ -376,32 +377,34 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
 #endif
           switch (cid >> 2) {                        // case id * 4 (jump-table offset)
             GP_ALL_CASES
-            case kCaseEndPass: {                     // next row pass of the same program
-              end_pass(cw);
-              ebase = (int)cw.z * NT * R + tid * 4;
-            } break;
-            case kCaseEnd: {                         // program done: warp-reduce into smem (A5)
-              end_pass(cw);
+            default: __builtin_unreachable();        // stage / pack guarantee a valid case
+          }
+          if (cw.w) {                                // last word of a row pass (pack_kernel)
+            end_pass();
+            if (cw.w & kEndPass) {                   // next row pass of the same program
+              ebase = (int)(cw.w >> 8) * NT * R + tid * 4;
+            } else {                                 // program done: warp-reduce into smem (A5)
               if constexpr (!PREDICT) {
-                double* slot = acc + ((size_t)warp * a.G + cw.z) * S;
+                const int j = (int)(cw.w >> 8);      // == pslot
                 if (S == 1) {
                   if (npend == 3) {                  // fourth program: one batched reduction
-                    reduce4(l0, (int)cw.z, 4);
+                    reduce4(l0, j, 4);
                     npend = 0;
                   } else {
                     pend0 = pend1; pend1 = pend2; pend2 = l0;
-                    pidx0 = pidx1; pidx1 = pidx2; pidx2 = (int)cw.z;
+                    pidx0 = pidx1; pidx1 = pidx2; pidx2 = j;
                     ++npend;
                   }
                 } else {
+                  double* slot = acc + ((size_t)warp * a.G + j) * S;
                   const double v0 = warp_sum_f64(l0), v1 = warp_sum_f64(l1), v2 = warp_sum_f64(l2);
                   if (lane == 0) { slot[0] += v0; slot[1] += v1; slot[2] += v2; }
                 }
                 l0 = l1 = l2 = 0.f;
               }
               ebase = tid * 4;
-            } break;
-            default: __builtin_unreachable();        // stage / pack guarantee a valid case
+              ++pslot;
+            }
           }
         }
       }
@@ -418,12 +421,11 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
     if constexpr (!PREDICT) {
       __syncthreads();
       double* prow = a.partial + q * a.ld_part;
-      const int32_t* __restrict__ ids = a.prog_ids + (int64_t)g * a.G;
       for (int j = tid; j < np * S; j += NT) {
         const int pl = j / S, k = j - pl * S;
         double sum = 0.0;
         for (int wv = 0; wv < NW; ++wv) sum += acc[((size_t)wv * a.G + pl) * S + k];
-        prow[(int64_t)ids[pl] * S + k] = sum;
+        prow[(int64_t)gids[pl] * S + k] = sum;
       }
     }
   }

@@ -17,17 +17,18 @@ constexpr int kTile = 2048;
 constexpr int kNumVariants = 4;
 constexpr int kVariantStack[kNumVariants] = {4, 8, 12, 20};
 
-// Stream marker cases (after every (op, variant, slot) case id).
-constexpr int kCaseEndPass = 123 * kCaseStride;   // OPV_COUNT * kCaseStride
-constexpr int kCaseEnd = kCaseEndPass + 1;
+// Pass flags in .w of the LAST code word of each row pass of a program in a code stream:
+// bits 0-1 = kEndPass (another pass follows; bits 8.. = its index) or kEndProgram (bits 8.. =
+// the program's slot in its group).
+constexpr uint32_t kEndPass = 1u, kEndProgram = 2u;
 // Code-stream window staged in shared memory per CTA (words of 16 B).
 constexpr int kStreamWin = 768;
 
 // Everything the fused evaluator needs for one launch (see eval_impl.cuh). Each variant runs a
 // packed CODE STREAM per program group: for every program of the group, SUB copies of its code
-// words (one per row pass) each followed by a marker word -- END_PASS {case, p, next pass, K_p} or
-// END {case, p, index within the group, K_p} -- so the evaluator walks one contiguous stream with
-// an uninterrupted prefetch and does the loss / reduction in the marker cases.
+// words (one per row pass), the last word of each pass flagged in .w -- so the evaluator walks one
+// contiguous stream with an uninterrupted prefetch and does the loss / reduction after the flagged
+// word, without a separate dispatch.
 struct EvalArgs {
   const uint4* stream;        // this variant's packed stream (+2 pad words)
   const int64_t* gstart;      // [n_groups + 1] stream offsets of the program groups
@@ -47,6 +48,7 @@ struct EvalArgs {
   int64_t n_chunks;           // row chunks; work items = ceil(count / G) * n_chunks
   double* partial;            // FIT: [n_chunks][ld_part], ld_part = n_programs * S + 3
   int64_t ld_part;
+  const float* shift;         // Pearson: K_p per program
   const float* y_shift;       // Pearson: device scalar K_y
   float* out;                 // PREDICT: out[p * ld_out + i]
   int64_t ld_out;
