@@ -134,7 +134,8 @@ def roofline_of(sfu, fp32, eval_ms, launches, step_ms):
     else:
         r = {"bound": "alu", "pipe": "FP32", "achieved": round(fp32 / eval_s / 1e12, 4),
              "peak": round(FP32_PEAK / 1e12, 4), "unit": "TFLOP/s (fp32)", "frac": round(f_fp32, 4)}
-    r.update({"traffic": ncu_traffic(), "sfu_frac": round(f_sfu, 4), "fp32_frac": round(f_fp32, 4),
+    r.update({"traffic": ncu_traffic(), "traffic_scope": "DRAM bytes of one evaluation's eval "
+              "launches (profiles/eval_kernel_ncu.json)", "sfu_frac": round(f_sfu, 4), "fp32_frac": round(f_fp32, 4),
               "eval_ms_per_launch": round(eval_ms / max(launches, 1), 3),
               "eval_share_of_step": round(eval_ms / step_ms, 4),
               "peak_note": "SFU: 148 SMs x 16 MUFU/clk x 1965 MHz (measured MUFU.SIN 4.63e12/s); "
@@ -147,7 +148,7 @@ def ncu_traffic():
     path = os.path.join(ROOT, "profiles", "eval_kernel_ncu.json")
     try:
         with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            return json.load(f).get("dram_bytes_per_launch")   # per evaluation (all variants)
     except Exception:
         return None
 
@@ -279,6 +280,12 @@ def run_b200(args, cfg):
         Xp = torch.from_numpy(Xh).pin_memory()
         yp = torch.from_numpy(yh).pin_memory()
         pop_bytes = 0
+        # a fresh engine with the same seed replays the SAME generations as the timed region
+        # (the engine is deterministic), so value and e2e price identical populations
+        eng = gp.Engine(ctx, X, y, **kw)
+        eng.init_population()
+        for _ in range(args.warmup):
+            eng.generation()
         barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -305,6 +312,8 @@ def run_b200(args, cfg):
     out = None
     if rank == 0:
         nodes, off, _ = eng.population()
+        if args.dump_population:
+            np.savez_compressed(args.dump_population, nodes=nodes, off=off)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(nodes, off, Xh, yh, cfg["metric"])
@@ -389,6 +398,8 @@ def main():
     ap.add_argument("--weak", action="store_true", help="per-GPU rows fixed (default: strong)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dump-population", default=None,
+                    help="save the final population (nodes, offsets) to this .npz (analysis)")
     ap.add_argument("--nccl", action="store_true",
                     help="use the NCCL communicator path even with one rank (plumbing check)")
     args = ap.parse_args()

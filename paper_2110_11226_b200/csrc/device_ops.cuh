@@ -134,6 +134,67 @@ __device__ __forceinline__ float apply1(float a) {
   else return atan_bf(a);  // GP_OP_ATAN
 }
 
+// ---- row pairs: Blackwell's packed fp32x2 pipe (FADD2 / FMUL2 / FFMA2) ---------------------------
+// Two rows per instruction for the ops whose scalar form is one correctly rounded add / mul / fma:
+// bit-identical to the scalar path (same rounding, same -ftz), half the issue slots. ptxas keeps
+// the row pairs of the register stack in aligned register pairs, so no packing moves are emitted.
+#define GPB_X2(OPC, d0, d1, a0, a1, b0, b1)                                                      \
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2,%3};\n\tmov.b64 b, {%4,%5};\n\t" OPC               \
+      " d, a, b;\n\tmov.b64 {%0,%1}, d;}"                                                        \
+      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1))
+__device__ __forceinline__ void add_x2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  GPB_X2("add.rn.ftz.f32x2", d0, d1, a0, a1, b0, b1);
+}
+__device__ __forceinline__ void sub_x2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  GPB_X2("sub.rn.ftz.f32x2", d0, d1, a0, a1, b0, b1);
+}
+__device__ __forceinline__ void mul_x2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  GPB_X2("mul.rn.ftz.f32x2", d0, d1, a0, a1, b0, b1);
+}
+// d = a * b + c on both lanes (one rounding, as fmaf)
+__device__ __forceinline__ void fma_x2(float& d0, float& d1, float a0, float a1, float b0, float b1,
+                                       float c0, float c1) {
+  asm("{.reg .b64 a, b, c, d;\n\tmov.b64 a, {%2,%3};\n\tmov.b64 b, {%4,%5};\n\t"
+      "mov.b64 c, {%6,%7};\n\tfma.rn.ftz.f32x2 d, a, b, c;\n\tmov.b64 {%0,%1}, d;}"
+      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+#undef GPB_X2
+
+// apply2 on two rows: (d0, d1) = (a0 OP b0, a1 OP b1), bit-identical to two apply2 calls.
+template <int OP>
+__device__ __forceinline__ void apply2_x2(float& d0, float& d1, float a0, float a1, float b0,
+                                          float b1) {
+  if constexpr (OP == GP_OP_ADD) add_x2(d0, d1, a0, a1, b0, b1);
+  else if constexpr (OP == GP_OP_SUB) sub_x2(d0, d1, a0, a1, b0, b1);
+  else if constexpr (OP == GP_OP_MUL) mul_x2(d0, d1, a0, a1, b0, b1);
+  else if constexpr (OP == GP_OP_DIV) {
+    float q0, q1;
+    mul_x2(q0, q1, a0, a1, rcp_approx(b0), rcp_approx(b1));
+    d0 = fabsf(b0) < kProt ? 1.0f : q0;
+    d1 = fabsf(b1) < kProt ? 1.0f : q1;
+  } else {
+    const float r0 = apply2<OP>(a0, b0), r1 = apply2<OP>(a1, b1);
+    d0 = r0;
+    d1 = r1;
+  }
+}
+// apply1 on two rows, bit-identical to two apply1 calls.
+template <int OP>
+__device__ __forceinline__ void apply1_x2(float& d0, float& d1, float a0, float a1) {
+  if constexpr (OP == GP_OP_SQUARE) mul_x2(d0, d1, a0, a1, a0, a1);
+  else if constexpr (OP == GP_OP_CUBE) {
+    float s0, s1;
+    mul_x2(s0, s1, a0, a1, a0, a1);
+    mul_x2(d0, d1, s0, s1, a0, a1);
+  } else if constexpr (OP == GP_OP_TAN) {
+    mul_x2(d0, d1, __sinf(a0), __sinf(a1), rcp_approx(__cosf(a0)), rcp_approx(__cosf(a1)));
+  } else {
+    const float r0 = apply1<OP>(a0), r1 = apply1<OP>(a1);
+    d0 = r0;
+    d1 = r1;
+  }
+}
+
 // Runtime-dispatched scalar version (used by the Pearson shift kernel: one row per program).
 __device__ __forceinline__ float apply_rt(int op, float a, float b) {
   switch (op) {

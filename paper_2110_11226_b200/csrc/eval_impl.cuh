@@ -103,6 +103,18 @@ __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
     { const int r = 4 * k + 3; const int j_ = 3; (void)j_; stmt; }                             \
   }
 #define GP_F4(v) (j_ == 0 ? v.x : j_ == 1 ? v.y : j_ == 2 ? v.z : v.w)
+// row pairs (r, r + 1): the FP32x2 forms of device_ops.cuh (apply2_x2 / apply1_x2)
+#define GP_PAIRS(stmt) _Pragma("unroll") for (int r = 0; r < R; r += 2) { stmt; }
+// for each 4-row chunk k: stmt on the pairs (4k, 4k+1) <- (v.x, v.y) and (4k+2, 4k+3) <- (v.z, v.w)
+#define GP_CHUNKS2(pre, stmt)                                                                  \
+  _Pragma("unroll") for (int k = 0; k < R4; ++k) {                                             \
+    pre;                                                                                       \
+    { const int r = 4 * k;     const int j_ = 0; (void)j_; stmt; }                             \
+    { const int r = 4 * k + 2; const int j_ = 1; (void)j_; stmt; }                             \
+  }
+#define GP_LO(v) (j_ == 0 ? v.x : v.z)
+#define GP_HI(v) (j_ == 0 ? v.y : v.w)
+#define GP_ST2(s) st[s][r], st[s][r + 1]
 
 #define GP_PUSH(s)                                                                             \
   case LBL(OPV_PUSH_V, s): { GP_CHUNKS(GP_VAR4(t, cw.y, k), st[s][r] = GP_F4(t)) } break;      \
@@ -110,30 +122,32 @@ __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
 
 // binary op OP at destination slot s; a = first operand, b = second operand
 #define GP_BIN_SS(OP, s)                                                                       \
-  case LBL(opv_bin(OP, BV_SS), s): { GP_ROWS(st[s][r] = apply2<OP>(st[(s) + 1][r], st[s][r])) } break; \
-  case LBL(opv_bin(OP, BV_SSR), s): { GP_ROWS(st[s][r] = apply2<OP>(st[s][r], st[(s) + 1][r])) } break;
+  case LBL(opv_bin(OP, BV_SS), s): {                                                           \
+    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), GP_ST2((s) + 1), GP_ST2(s))) } break;                    \
+  case LBL(opv_bin(OP, BV_SSR), s): {                                                          \
+    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), GP_ST2(s), GP_ST2((s) + 1))) } break;
 #define GP_BIN_T(OP, s)                                                                        \
   case LBL(opv_bin(OP, BV_SV), s): {                                                           \
-    GP_CHUNKS(GP_VAR4(t, cw.z, k), st[s][r] = apply2<OP>(st[s][r], GP_F4(t))) } break;         \
+    GP_CHUNKS2(GP_VAR4(t, cw.z, k), apply2_x2<OP>(GP_ST2(s), GP_ST2(s), GP_LO(t), GP_HI(t))) } break; \
   case LBL(opv_bin(OP, BV_SC), s): { const float c = GP_CONST(cw.z);                           \
-    GP_ROWS(st[s][r] = apply2<OP>(st[s][r], c)) } break;                                       \
+    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), GP_ST2(s), c, c)) } break;                               \
   case LBL(opv_bin(OP, BV_VS), s): {                                                           \
-    GP_CHUNKS(GP_VAR4(t, cw.y, k), st[s][r] = apply2<OP>(GP_F4(t), st[s][r])) } break;         \
+    GP_CHUNKS2(GP_VAR4(t, cw.y, k), apply2_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t), GP_ST2(s))) } break; \
   case LBL(opv_bin(OP, BV_CS), s): { const float c = GP_CONST(cw.y);                           \
-    GP_ROWS(st[s][r] = apply2<OP>(c, st[s][r])) } break;                                       \
+    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), c, c, GP_ST2(s))) } break;                               \
   case LBL(opv_bin(OP, BV_VV), s): {                                                           \
-    GP_CHUNKS(GP_VAR4(t, cw.y, k) GP_VAR4(u, cw.z, k),                                         \
-              st[s][r] = apply2<OP>(GP_F4(t), GP_F4(u))) } break;                              \
+    GP_CHUNKS2(GP_VAR4(t, cw.y, k) GP_VAR4(u, cw.z, k),                                        \
+               apply2_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t), GP_LO(u), GP_HI(u))) } break;      \
   case LBL(opv_bin(OP, BV_VC), s): { const float c = GP_CONST(cw.z);                           \
-    GP_CHUNKS(GP_VAR4(t, cw.y, k), st[s][r] = apply2<OP>(GP_F4(t), c)) } break;                \
+    GP_CHUNKS2(GP_VAR4(t, cw.y, k), apply2_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t), c, c)) } break; \
   case LBL(opv_bin(OP, BV_CV), s): { const float c = GP_CONST(cw.y);                           \
-    GP_CHUNKS(GP_VAR4(u, cw.z, k), st[s][r] = apply2<OP>(c, GP_F4(u))) } break;                \
+    GP_CHUNKS2(GP_VAR4(u, cw.z, k), apply2_x2<OP>(GP_ST2(s), c, c, GP_LO(u), GP_HI(u))) } break; \
   case LBL(opv_bin(OP, BV_CC), s): {                                                           \
     const float v = apply2<OP>(GP_CONST(cw.y), GP_CONST(cw.z)); GP_ROWS(st[s][r] = v) } break;
 #define GP_UN(OP, s)                                                                           \
-  case LBL(opv_un(OP, UV_S), s): { GP_ROWS(st[s][r] = apply1<OP>(st[s][r])) } break;           \
+  case LBL(opv_un(OP, UV_S), s): { GP_PAIRS(apply1_x2<OP>(GP_ST2(s), GP_ST2(s))) } break;      \
   case LBL(opv_un(OP, UV_V), s): {                                                             \
-    GP_CHUNKS(GP_VAR4(t, cw.y, k), st[s][r] = apply1<OP>(GP_F4(t))) } break;                   \
+    GP_CHUNKS2(GP_VAR4(t, cw.y, k), apply1_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t))) } break;     \
   case LBL(opv_un(OP, UV_C), s): { const float v = apply1<OP>(GP_CONST(cw.y));                 \
     GP_ROWS(st[s][r] = v) } break;
 
@@ -281,12 +295,11 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
 #pragma unroll
           for (int k = 0; k < R4; ++k) {
             const float4 yv = *reinterpret_cast<const float4*>(ys + ebase + k * NT * 4);
-            const float yy[4] = {yv.x, yv.y, yv.z, yv.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float d = st[0][4 * k + j] - yy[j];
-              l0 = fmaf(d, d, l0);
-            }
+            float d0, d1, d2, d3;
+            sub_x2(d0, d1, st[0][4 * k], st[0][4 * k + 1], yv.x, yv.y);
+            sub_x2(d2, d3, st[0][4 * k + 2], st[0][4 * k + 3], yv.z, yv.w);
+            fma_x2(l0, l1, d0, d1, d0, d1, l0, l1);  // even / odd rows: l1 joins l0 at the end
+            fma_x2(l0, l1, d2, d3, d2, d3, l0, l1);
           }
           return;
         }
@@ -387,11 +400,12 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
               if constexpr (!PREDICT) {
                 const int j = (int)(cw.w >> 8);      // == pslot
                 if (S == 1) {
+                  const float lp = l0 + l1;          // l1: odd rows of the paired MSE path
                   if (npend == 3) {                  // fourth program: one batched reduction
-                    reduce4(l0, j, 4);
+                    reduce4(lp, j, 4);
                     npend = 0;
                   } else {
-                    pend0 = pend1; pend1 = pend2; pend2 = l0;
+                    pend0 = pend1; pend1 = pend2; pend2 = lp;
                     pidx0 = pidx1; pidx1 = pidx2; pidx2 = j;
                     ++npend;
                   }

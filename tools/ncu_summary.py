@@ -45,24 +45,39 @@ def full(rep, out):
                                  for h in hdr if h.startswith(STALLS) and h.endswith(
                                      "_per_issue_active.ratio") and d[h] not in ("", "0")}
         kernels.append((k, d, u))
-    k, d, u = kernels[0]
-
-    def val(key, scale):
+    def val(d, u, key):
         v, un = float(d[key].replace(",", "")), u[key]
-        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(un, 1)
-        return v * mult / scale
+        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(un, 1)
 
-    dram = val("dram__bytes_read.sum", 1) + val("dram__bytes_write.sum", 1)
-    summary = {"report": rep, "kernel": k["kernel"], "dram_bytes_per_launch": dram, "metrics": k}
+    def ms(d, u):
+        v, un = float(d["gpu__time_duration.sum"].replace(",", "")), u["gpu__time_duration.sum"]
+        return v * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1, "second": 1e3}.get(un, 1)
+
+    per = []
+    for k, d, u in kernels:
+        k["dram_bytes"] = val(d, u, "dram__bytes_read.sum") + val(d, u, "dram__bytes_write.sum")
+        k["ms"] = ms(d, u)
+        per.append(k)
+    dram = sum(k["dram_bytes"] for k in per)
+    # the captured launches are the eval-kernel launches of ONE evaluation (one per non-empty
+    # stack-need variant): their summed DRAM traffic is the traffic of one evaluation
+    summary = {"report": rep, "kernels": [k["kernel"] for k in per],
+               "dram_bytes_per_launch": dram, "traffic_scope": "one evaluation (sum over the "
+               "captured eval-kernel launches)", "per_kernel": per}
     json.dump(summary, open(out + ".json", "w"), indent=1)
     with open(out + ".md", "w") as f:
-        f.write(f"# ncu --set full: {k['kernel']}\n\nsource report: `{rep}`\n\n| metric | value |\n|---|---|\n")
-        for key in KEYS:
-            if key in k:
-                f.write(f"| {key} | {k[key]} |\n")
-        f.write(f"| dram bytes per launch (read+write) | {dram:.4g} B |\n\n## stall reasons (warps per issue)\n\n")
-        for s, v in sorted(k["stalls_per_issue"].items(), key=lambda x: -float(x[1])):
-            f.write(f"- {s}: {float(v):.3f}\n")
+        f.write(f"# ncu --set full\n\nsource report: `{rep}`\n\n"
+                f"DRAM read+write summed over the {len(per)} captured launches: {dram:.4g} B\n\n")
+        for k in per:
+            f.write(f"## {k['kernel']}\n\n| metric | value |\n|---|---|\n")
+            for key in KEYS:
+                if key in k:
+                    f.write(f"| {key} | {k[key]} |\n")
+            f.write(f"| dram bytes (read+write) | {k['dram_bytes']:.4g} B |\n\n"
+                    "stall reasons (warps per issue):\n\n")
+            for s, v in sorted(k["stalls_per_issue"].items(), key=lambda x: -float(x[1]))[:12]:
+                f.write(f"- {s}: {float(v):.3f}\n")
+            f.write("\n")
     print(open(out + ".md").read())
 
 
