@@ -1,0 +1,8 @@
+# Round-1 (second session) GPU pass: parity tests, smoke, bench C3, launch list, ncu --set full of the evaluator.
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_c3.log 2>&1; tail -1 gpurun_out/bench_c3.log > gpurun_out/bench_r01_v10_c3.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_v10.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:eval_kernel --launch-skip 10 --launch-count 2 -f -o gpurun_out/prof_r01_v10 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/prof.log 2>&1
