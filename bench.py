@@ -116,11 +116,20 @@ class ClockSampler:
                 else None, "reasons": reasons, "samples": len(self.rows)}
 
 
-def algorithmic_ops(op_count, rows, metric, n_programs):
+# metrics whose variable-free programs get their fitness from the dataset moments (no per-row
+# loss; gp_context_set_const_programs)
+CLOSED_FORM_METRICS = ("mse", "rmse", "pearson")
+
+
+def algorithmic_ops(op_count, rows, metric, n_programs, const_programs=0):
+    """Per-row algorithmic work of one evaluation: SFU / FP32 ops of the variable-dependent nodes
+    plus the loss of every program evaluated per row (constant programs under a closed-form
+    metric have no per-row loss)."""
     sfu = sum(SFU_COST.get(op, 0) * c for op, c in enumerate(op_count)) * rows
     fp32 = sum(FP32_COST.get(op, 0) * c for op, c in enumerate(op_count)) * rows
-    sfu += LOSS_SFU.get(metric, 0) * n_programs * rows
-    fp32 += LOSS_FP32[metric] * n_programs * rows
+    per_row = n_programs - (const_programs if metric in CLOSED_FORM_METRICS else 0)
+    sfu += LOSS_SFU.get(metric, 0) * per_row * rows
+    fp32 += LOSS_FP32[metric] * per_row * rows
     return sfu, fp32
 
 
@@ -195,6 +204,7 @@ def run_b200(args, cfg):
         uid = obj[0]
     stream = torch.cuda.Stream(local)
     ctx = gp.Context(local, stream=stream, unique_id=uid, rank=rank, world_size=world)
+    ctx.set_const_programs(not args.no_const_programs)
     Xh, yh, x0, y0, m_global = load_dataset(cfg, rank, world)
     ctx.set_reference_row(x0, y0)
     X = torch.from_numpy(Xh).cuda(local)
@@ -205,7 +215,7 @@ def run_b200(args, cfg):
     eng = gp.Engine(ctx, X, y, **kw)
     st0 = eng.init_population()
     n0, o0, _ = eng.population()
-    gen0 = (n0, o0, st0["op_count"])
+    gen0 = (n0, o0, st0["op_count"], st0["const_programs"])
     for _ in range(args.warmup):
         eng.generation()
 
@@ -244,7 +254,8 @@ def run_b200(args, cfg):
     rows_local = X.shape[1]
     sfu = fp32 = 0
     for s in steps:
-        a, b2 = algorithmic_ops(s["op_count"], rows_local, cfg["metric"], cfg["pop"])
+        a, b2 = algorithmic_ops(s["op_count"], rows_local, cfg["metric"], cfg["pop"],
+                                0 if args.no_const_programs else s["const_programs"])
         sfu, fp32 = sfu + a, fp32 + b2
     roofline = roofline_of(sfu, fp32, eval_ms, eval_launches, ms)
     var_nodes = sum(sum(s["op_count"]) for s in steps) * m_global
@@ -254,7 +265,7 @@ def run_b200(args, cfg):
     # more per-row transcendental work than evolved populations: a capability point
     roof0 = None
     if gen0 is not None:
-        n0, o0, ops0 = gen0
+        n0, o0, ops0, cp0 = gen0
         nd, of = torch.from_numpy(n0).cuda(local), torch.from_numpy(o0).cuda(local)
         fit_buf = torch.empty(len(o0) - 1, dtype=torch.float32, device=f"cuda:{local}")
         for _ in range(2):
@@ -268,7 +279,8 @@ def run_b200(args, cfg):
         torch.cuda.synchronize()
         ms0, l0 = ctx.eval_timing(reset=True)
         ctx.set_profiling(False)
-        a0, b0 = algorithmic_ops(ops0, rows_local, cfg["metric"], cfg["pop"])
+        a0, b0 = algorithmic_ops(ops0, rows_local, cfg["metric"], cfg["pop"],
+                                 0 if args.no_const_programs else cp0)
         roof0 = roofline_of(a0 * reps, b0 * reps, ms0, l0, ms0)
         roof0["node_evals_per_s"] = float(len(n0)) * rows_local * reps / (ms0 * 1e-3)
         roof0["population"] = "generation 0 (ramped half-and-half), mean length %.2f" % (
@@ -330,6 +342,8 @@ def run_b200(args, cfg):
                        "l2": "inputs larger than L2 (X + y = %.0f MB)" % ((Xh.nbytes + yh.nbytes) * world / 1e6)},
             "roofline": roofline, "roofline_gen0": roof0,
             "var_node_evals_per_s": var_nodes / (ms * 1e-3), "const_node_share": round(const_share, 4),
+            "const_program_share": round(float(np.mean([s["const_programs"] / cfg["pop"] for s in steps])), 4),
+            "const_programs_closed_form": (not args.no_const_programs) and cfg["metric"] in CLOSED_FORM_METRICS,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
@@ -398,6 +412,8 @@ def main():
     ap.add_argument("--weak", action="store_true", help="per-GPU rows fixed (default: strong)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-const-programs", action="store_true",
+                    help="evaluate variable-free programs per row (no closed-form fitness)")
     ap.add_argument("--dump-population", default=None,
                     help="save the final population (nodes, offsets) to this .npz (analysis)")
     ap.add_argument("--nccl", action="store_true",

@@ -140,6 +140,15 @@ gp_status gp_context_eval_timing(gp_context* ctx, double* total_ms, int64_t* lau
  * (second operand first). Results are identical either way (same operations on the same
  * operands); only the stack need, hence the evaluator variant a program runs in, changes. */
 gp_status gp_context_set_eval_order(gp_context* ctx, int sethi_ullman);
+/* Variable-free programs: a program whose whole tree folds to one constant c at compile time
+ * (stage kernel) predicts c on every row. With closed_form = 1 (default) gp_evaluate takes its
+ * MSE / RMSE sum from the dataset moments, sum_i w_i (c - y_i)^2 = W c^2 - 2 c S_y + S_yy
+ * (fp64, the same per-chunk W, S_y, S_yy the Pearson path uses), and reports its Pearson
+ * correlation as undefined (0, GP_FLAG_UNDEFINED_CORR) -- both without a per-row pass. This is
+ * the per-row loss of P:256-262 with the constant prediction factored out of the sum. MAE and
+ * LogLoss still evaluate such programs per row. 0: every program goes through the per-row
+ * evaluator. */
+gp_status gp_context_set_const_programs(gp_context* ctx, int closed_form);
 /* Number of CUDA kernels this context has launched (all entry points) since the last reset. */
 gp_status gp_context_kernel_launches(gp_context* ctx, int64_t* launches, int reset);
 
@@ -244,6 +253,7 @@ typedef struct {
   int64_t op_count[GP_OP_COUNT]; /* opcode histogram of the evaluated population's nodes whose
                                    subtree contains a variable (per-row work) */
   int64_t const_nodes;           /* nodes of variable-free subtrees (per-program constants) */
+  int64_t const_programs;        /* programs whose whole tree is variable-free */
 } gp_generation_stats;
 
 /* Creates an engine over a dataset. X / y / w are [host|device] (same layouts as gp_evaluate);

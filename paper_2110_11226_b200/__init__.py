@@ -126,6 +126,12 @@ class Context:
                                             int(reset)), self.handle, "eval_timing")
         return ms.value, n.value
 
+    def set_const_programs(self, closed_form: bool = True):
+        """gp_context_set_const_programs: variable-free programs' MSE / RMSE / Pearson fitness from
+        the dataset moments (default) or through the per-row evaluator."""
+        _check(lib().gp_context_set_const_programs(self.handle, int(bool(closed_form))), self.handle,
+               "set_const_programs")
+
     def set_eval_order(self, sethi_ullman: bool = True):
         """Sethi-Ullman operand order (default) or the classic reverse-prefix order."""
         _check(lib().gp_context_set_eval_order(self.handle, int(bool(sethi_ullman))), self.handle,

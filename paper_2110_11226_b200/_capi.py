@@ -28,6 +28,7 @@ SIGNATURES = {
                                ctypes.c_int),
     "gp_context_kernel_launches": ([P, ctypes.POINTER(i64), ctypes.c_int], ctypes.c_int),
     "gp_context_set_eval_order": ([P, ctypes.c_int], ctypes.c_int),
+    "gp_context_set_const_programs": ([P, ctypes.c_int], ctypes.c_int),
     "gp_evaluate": ([P, P, P, i32, i64, i32, P, i64, P, P, i64, i32, ctypes.c_int, P, P],
                     ctypes.c_int),
     "gp_predict": ([P, P, P, i32, i64, i32, P, i64, i64, i32, P, i64, P], ctypes.c_int),
@@ -63,7 +64,7 @@ class GpGenerationStats(ctypes.Structure):
         ("best_len", i32), ("best_depth", i32), ("mean_raw", f64), ("total_nodes", i64),
         ("max_stack_need", i32), ("n_tournaments", i32), ("t_select_s", f64),
         ("t_mutate_s", f64), ("t_h2d_s", f64), ("t_eval_s", f64), ("t_total_s", f64),
-        ("op_count", i64 * 26), ("const_nodes", i64),
+        ("op_count", i64 * 26), ("const_nodes", i64), ("const_programs", i64),
     ]
 
     def as_dict(self):

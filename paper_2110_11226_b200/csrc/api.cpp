@@ -136,7 +136,8 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   pl.n_groups = n_groups;
   pl.n_chunks = Q;
   pl.rows_per_chunk = tpc * tile;
-  const size_t acc = predict ? 0 : (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15);
+  const size_t acc = predict ? 0 : (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15) +
+                                    (size_t)kRedBytes;
   const size_t yw = predict ? 0 : (weighted ? 2 : 1) * (size_t)tile * sizeof(float);
   pl.smem = acc + yw + (pl.xsmem ? (size_t)n_cols * tile * sizeof(float) : 0) +
             (size_t)(kStreamWin + 2) * 16;
@@ -291,6 +292,12 @@ gp_status gp_context_eval_timing(gp_context* ctx, double* total_ms, int64_t* lau
   return GP_OK;
 }
 
+gp_status gp_context_set_const_programs(gp_context* ctx, int closed_form) {
+  if (!ctx) return GP_ERR_ARG;
+  ctx->const_programs = closed_form != 0;
+  return GP_OK;
+}
+
 gp_status gp_context_set_eval_order(gp_context* ctx, int sethi_ullman) {
   if (!ctx) return GP_ERR_ARG;
   ctx->sethi_ullman = sethi_ullman != 0;
@@ -323,7 +330,7 @@ gp_status gp_context_set_reference_row(gp_context* ctx, const float* x_ref, int3
 static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_t*& offsets,
                          int32_t n_programs, int64_t n_nodes, int32_t max_stack, const float*& X,
                          int64_t ldx, int64_t n_rows, int32_t n_cols, int32_t G, bool pearson,
-                         const float* y, bool* any_host) {
+                         const float* y, bool* any_host, bool skip_const = false) {
   if (n_programs < 1 || n_nodes < 1 || max_stack < 1 || max_stack > GP_MAX_STACK || n_rows < 1 ||
       n_cols < 1 || ldx < n_rows || !programs || !offsets || !X)
     return ctx->fail(GP_ERR_ARG, "invalid argument (n_programs=%d n_nodes=%lld max_stack=%d "
@@ -384,11 +391,13 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   for (int v = 0; v < kNumVariants; ++v) subs[v] = variant(v).shape.SUB;
   if ((s = ctx->launch(launch_bucket((const int32_t*)ctx->need.p, (const int32_t*)ctx->code_len.p,
                                    n_programs, G, subs, (int32_t*)ctx->lists.p, (int64_t*)ctx->pos.p,
-                                   (int64_t*)ctx->gstart.p, counts, base, ctx->stream),
+                                   (int64_t*)ctx->gstart.p, counts, base, skip_const ? 1 : 0,
+                                   ctx->stream),
                      "bucket kernel"))) return s;
   return ctx->launch(launch_pack((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
                                (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->lists.p,
-                               (const int64_t*)ctx->pos.p, counts, base, n_programs, G, subs,
+                               (const int64_t*)ctx->pos.p, counts, base,
+                               (const int64_t*)ctx->gstart.p, n_programs, G, subs,
                                (uint4*)ctx->codestream.p, ctx->stream),
                    "pack kernel");
 }
@@ -416,8 +425,11 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
   const bool st_host = status_out && is_host_pointer(status_out);
   const int S = metric == GP_PEARSON ? 3 : 1;
   const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, S, false, w != nullptr);
+  // variable-free programs: closed form in finalize for MSE / RMSE / Pearson (not MAE, LogLoss)
+  const bool closed = ctx->const_programs &&
+                      (metric == GP_MSE || metric == GP_RMSE || metric == GP_PEARSON);
   if ((s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, n_rows,
-                   n_cols, pl.G, metric == GP_PEARSON, y, &any_host))) return s;
+                   n_cols, pl.G, metric == GP_PEARSON, y, &any_host, closed))) return s;
 
   // Fused evaluation -> partial sums
   const int64_t ld_part = (int64_t)n_programs * S + 3;
@@ -460,7 +472,9 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
     fit_dev = (float*)ctx->h_fit.p;
   }
   if ((s = ctx->launch(launch_finalize((const double*)ctx->sums.p, n_programs, metric,
-                                     (const int32_t*)ctx->code_len.p, fit_dev,
+                                     (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->need.p,
+                                     (const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
+                                     closed ? 1 : 0, fit_dev,
                                      (uint32_t*)ctx->status.p, ctx->stream), "finalize"))) return s;
   if (fit_host) {
     if ((s = ctx->cuda(cudaMemcpyAsync(fitness_out, fit_dev, (size_t)n_programs * sizeof(float),

@@ -20,7 +20,8 @@ namespace gpb {
 //    a post-order emission then writes one code word per function node with its static
 //    destination slot (device_ops.cuh "compiled program code"); stack need > capacity ->
 //    GP_FLAG_STACK_OVERFLOW. Depth > 127 is also reported as overflow.
-// Invalid programs get code_len = 0 and are skipped by every later kernel.
+// Invalid programs get code_len = 0 and are skipped by every later kernel. Variable-free programs
+// (the whole tree folds to one constant) get need = 0.
 // ---------------------------------------------------------------------------------------------
 __global__ void stage_kernel(const gp_node* __restrict__ nodes, const int64_t* __restrict__ off,
                              int32_t n_programs, int64_t n_nodes, int32_t n_cols, int32_t cap,
@@ -100,6 +101,9 @@ __global__ void stage_kernel(const gp_node* __restrict__ nodes, const int64_t* _
     }
     need_root = (len == 1 || nd_cst[0]) ? 1 : nd_need[0];
     if (need_root > cap) flags |= GP_FLAG_STACK_OVERFLOW;
+    // a variable-free program is ONE constant c (its single PUSH_C word carries c): need 0 marks
+    // it, so its loss can come from the dataset moments (finalize_kernel) instead of per row
+    if (nd_cst[0]) need_root = 0;
   }
   if (!flags) {
     // (2) post-order emission with the chosen child order; terminal and folded-constant operands
@@ -116,7 +120,7 @@ __global__ void stage_kernel(const gp_node* __restrict__ nodes, const int64_t* _
       return 0;
     };
     auto emit = [&](int opv, int slot, uint32_t pa, uint32_t pb) {
-      code[b + emitted++] = make_uint4((uint32_t)(opv * kCaseStride + slot) * 4u, pa, pb, 0u);
+      code[b + emitted++] = make_uint4((uint32_t)(opv * kCaseStride + slot), pa, pb, 0u);
     };
     if (e - b == 1 || nd_cst[0]) {
       uint32_t pl;
@@ -237,7 +241,8 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
                                                       int64_t* __restrict__ pos,
                                                       int64_t* __restrict__ gstart,
                                                       int32_t* __restrict__ counts,
-                                                      int64_t* __restrict__ base, int4 sub4) {
+                                                      int64_t* __restrict__ base, int4 sub4,
+                                                      int32_t skip_const) {
   __shared__ int warp_cnt[kNumVariants][32];
   __shared__ int cnt[kNumVariants];
   __shared__ int64_t warp_tot[32];
@@ -250,7 +255,7 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
   for (int c0 = 0; c0 < n; c0 += 1024) {
     const int p = c0 + tid;
     int b = -1;
-    if (p < n && code_len[p] > 0) {
+    if (p < n && code_len[p] > 0 && !(skip_const && need[p] == 0)) {
       b = kNumVariants - 1;
       for (int v = kNumVariants - 1; v >= 0; --v)
         if (need[p] <= caps[v]) b = v;
@@ -300,9 +305,10 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
 
 cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
                           int32_t G, const int* subs, int32_t* lists, int64_t* pos,
-                          int64_t* gstart, int32_t* counts, int64_t* base, cudaStream_t s) {
+                          int64_t* gstart, int32_t* counts, int64_t* base, int32_t skip_const,
+                          cudaStream_t s) {
   bucket_kernel<<<1, 1024, 0, s>>>(need, code_len, n_programs, G, lists, pos, gstart, counts,
-                                   base, make_int4(subs[0], subs[1], subs[2], subs[3]));
+                                   base, make_int4(subs[0], subs[1], subs[2], subs[3]), skip_const);
   return cudaGetLastError();
 }
 
@@ -312,8 +318,8 @@ cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t 
 __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __restrict__ code_off,
                             const int32_t* __restrict__ code_len, const int32_t* __restrict__ lists,
                             const int64_t* __restrict__ pos, const int32_t* __restrict__ counts,
-                            const int64_t* __restrict__ base, int32_t n, int32_t G, int4 sub4,
-                            uint4* __restrict__ stream) {
+                            const int64_t* __restrict__ base, const int64_t* __restrict__ gstart,
+                            int32_t n, int32_t G, int4 sub4, uint4* __restrict__ stream) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) stream[base[kNumVariants]] = stream[base[kNumVariants] + 1] = make_uint4(0, 0, 0, 0);
   if (i >= (int64_t)kNumVariants * n) return;
@@ -324,22 +330,26 @@ __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __res
   const int len = code_len[p];
   const uint4* src = code + code_off[p];
   uint4* dst = stream + pos[i];
+  // the group's stream [gs, ge): words at window ends get kEndWin
+  const int64_t gs = gstart[(int64_t)b * (n + 1) + j / G], ge = gstart[(int64_t)b * (n + 1) + j / G + 1];
   for (int pass = 0; pass < subs[b]; ++pass) {
     for (int k = 0; k < len; ++k) *dst++ = src[k];
     const bool last = pass == subs[b] - 1;
     dst[-1].w = last ? (kEndProgram | ((uint32_t)(j % G) << 8))
                      : (kEndPass | ((uint32_t)(pass + 1) << 8));
   }
+  for (int64_t t = pos[i] - gs; t < pos[i] - gs + (int64_t)subs[b] * len; ++t)
+    if ((t + 1) % kStreamWin == 0 || gs + t + 1 == ge) stream[gs + t].w |= kEndWin;
 }
 
 cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                         const int32_t* lists, const int64_t* pos, const int32_t* counts,
-                        const int64_t* base, int32_t n_programs, int32_t G, const int* subs,
-                        uint4* stream, cudaStream_t s) {
+                        const int64_t* base, const int64_t* gstart, int32_t n_programs,
+                        int32_t G, const int* subs, uint4* stream, cudaStream_t s) {
   const int nt = 256;
   const int64_t total = (int64_t)kNumVariants * n_programs;
   pack_kernel<<<(unsigned)((total + nt - 1) / nt), nt, 0, s>>>(code, code_off, code_len, lists,
-                                                               pos, counts, base,
+                                                               pos, counts, base, gstart,
                                                                n_programs, G,
                                                                make_int4(subs[0], subs[1], subs[2],
                                                                          subs[3]),
@@ -404,7 +414,7 @@ __global__ void shift_kernel(const uint4* __restrict__ code, const int64_t* __re
   };
   for (int k = 0; k < len; ++k) {
     const uint4 cw = pc[k];
-    const int id = (int)(cw.x >> 2), opv = id / kCaseStride, slot = id - opv * kCaseStride;
+    const int id = (int)cw.x, opv = id / kCaseStride, slot = id - opv * kCaseStride;
     if (opv < OPV_BIN0) {
       stk[slot] = term(opv == OPV_PUSH_V ? 1 : 2, cw.y);
     } else if (opv < OPV_UN0) {
@@ -472,6 +482,8 @@ cudaError_t launch_tile_reduce(const double* partial, int64_t n_chunks, int64_t 
 // ---------------------------------------------------------------------------------------------
 __global__ void finalize_kernel(const double* __restrict__ sums, int32_t n_programs,
                                 int32_t metric, const int32_t* __restrict__ code_len,
+                                const int32_t* __restrict__ need, const uint4* __restrict__ code,
+                                const int64_t* __restrict__ code_off, int32_t closed_const,
                                 float* __restrict__ fitness, uint32_t* __restrict__ status) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_programs) return;
@@ -480,16 +492,27 @@ __global__ void finalize_kernel(const double* __restrict__ sums, int32_t n_progr
   const double W = sums[nS], Sy = sums[nS + 1], Syy = sums[nS + 2];
   uint32_t fl = status[p];
   float out;
+  // closed_const: variable-free programs (need 0) were not evaluated per row; their sums follow
+  // from the dataset moments (consts_kernel, K_y = 0 for MSE): sum w (c - y)^2 =
+  // W c^2 - 2 c S_y + S_yy, and a constant prediction has an undefined Pearson correlation
+  const bool cst = closed_const && code_len[p] > 0 && need[p] == 0;
   if (code_len[p] == 0) {
     out = metric == GP_PEARSON ? -INFINITY : INFINITY;
   } else if (metric != GP_PEARSON) {
-    double f = sums[p] / W;
+    double f;
+    if (cst) {
+      const double c = (double)__uint_as_float(code[code_off[p]].y);
+      f = (W * c * c - 2.0 * c * Sy + Syy) / W;
+      if (f < 0.0) f = 0.0;                        // rounding; NaN / inf pass through
+    } else {
+      f = sums[p] / W;
+    }
     if (metric == GP_RMSE) f = sqrt(f);
     if (!isfinite(f) || f > (double)FLT_MAX) { f = INFINITY; fl |= GP_FLAG_NONFINITE; }
     out = (float)f;
   } else {
-    const double Sd = sums[3 * (int64_t)p], Sdd = sums[3 * (int64_t)p + 1],
-                 Sdy = sums[3 * (int64_t)p + 2];
+    const double Sd = cst ? 0.0 : sums[3 * (int64_t)p], Sdd = cst ? 0.0 : sums[3 * (int64_t)p + 1],
+                 Sdy = cst ? 0.0 : sums[3 * (int64_t)p + 2];
     const double cov = Sdy - Sd * Sy / W, vd = Sdd - Sd * Sd / W, vy = Syy - Sy * Sy / W;
     double r = cov / sqrt(vd * vy);
     if (!(vd > 0.0) || !(vy > 0.0) || !isfinite(r)) { r = 0.0; fl |= GP_FLAG_UNDEFINED_CORR; }
@@ -501,10 +524,12 @@ __global__ void finalize_kernel(const double* __restrict__ sums, int32_t n_progr
 }
 
 cudaError_t launch_finalize(const double* sums, int32_t n_programs, int32_t metric,
-                            const int32_t* code_len, float* fitness, uint32_t* status,
-                            cudaStream_t s) {
+                            const int32_t* code_len, const int32_t* need, const uint4* code,
+                            const int64_t* code_off, int32_t closed_const, float* fitness,
+                            uint32_t* status, cudaStream_t s) {
   const int nt = 128;
   finalize_kernel<<<(n_programs + nt - 1) / nt, nt, 0, s>>>(sums, n_programs, metric, code_len,
+                                                             need, code, code_off, closed_const,
                                                              fitness, status);
   return cudaGetLastError();
 }

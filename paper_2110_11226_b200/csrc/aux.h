@@ -18,12 +18,14 @@ cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n
 // counts: [kNumVariants] then counters [kNumVariants]; base: [kNumVariants + 1] stream bases.
 cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
                           int32_t G, const int* subs, int32_t* lists, int64_t* pos,
-                          int64_t* gstart, int32_t* counts, int64_t* base, cudaStream_t s);
-// Copies every bucketed program's code into its variant stream, flagging the end of each pass.
+                          int64_t* gstart, int32_t* counts, int64_t* base, int32_t skip_const,
+                          cudaStream_t s);
+// Copies every bucketed program's code into its variant stream, flagging the end of each pass
+// and of each shared-memory stream window (kernels.h kEndWin).
 cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                         const int32_t* lists, const int64_t* pos, const int32_t* counts,
-                        const int64_t* base, int32_t n_programs, int32_t G, const int* subs,
-                        uint4* stream, cudaStream_t s);
+                        const int64_t* base, const int64_t* gstart, int32_t n_programs,
+                        int32_t G, const int* subs, uint4* stream, cudaStream_t s);
 // Dataset constants W, S_y, S_yy per row chunk -> partial[q][col0 .. col0 + 2].
 cudaError_t launch_consts(const float* y, const float* w, int64_t n_rows, int64_t rows_per_chunk,
                           int64_t n_chunks, const float* y_shift, double* partial, int64_t ld_part,
@@ -33,9 +35,12 @@ cudaError_t launch_shift(const uint4* code, const int64_t* code_off, const int32
                          int64_t xref_stride, float* shift_out, cudaStream_t s);
 cudaError_t launch_tile_reduce(const double* partial, int64_t n_chunks, int64_t ld_part,
                                double* sums, cudaStream_t s);
+// closed_const: variable-free programs (need 0) skipped by the evaluator get their loss from the
+// dataset moments (MSE / RMSE) or an undefined correlation (Pearson).
 cudaError_t launch_finalize(const double* sums, int32_t n_programs, int32_t metric,
-                            const int32_t* code_len, float* fitness, uint32_t* status,
-                            cudaStream_t s);
+                            const int32_t* code_len, const int32_t* need, const uint4* code,
+                            const int64_t* code_off, int32_t closed_const, float* fitness,
+                            uint32_t* status, cudaStream_t s);
 cudaError_t launch_select(const float* fitness, const int64_t* offsets, int32_t n_programs,
                           int32_t n_tournaments, int32_t k, float parsimony, int32_t higher,
                           uint64_t seed, uint32_t generation, int32_t* winners, cudaStream_t s);

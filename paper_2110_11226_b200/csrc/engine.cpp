@@ -236,6 +236,7 @@ struct gp_engine {
   int max_need = 1;
   int64_t op_count[GP_OP_COUNT] = {};
   int64_t const_nodes = 0;
+  int64_t const_programs = 0;
   // flat CSR (pinned host) and its device copy
   gp_node* h_nodes = nullptr;
   int64_t* h_off = nullptr;
@@ -329,6 +330,7 @@ struct gp_engine {
     // per-program constants and are counted separately
     std::fill(op_count, op_count + GP_OP_COUNT, (int64_t)0);
     const_nodes = 0;
+    const_programs = 0;
     std::vector<char> is_const;
     for (int p = 0; p < n; ++p) {
       const Prog& pr = pop[p];
@@ -347,6 +349,7 @@ struct gp_engine {
         if (c) ++const_nodes;
         else if (op >= 0 && op < GP_OP_COUNT) ++op_count[op];
       }
+      if (!pr.empty() && is_const[0]) ++const_programs;
     }
     n_nodes = total;
     gp_status s;
@@ -390,6 +393,7 @@ struct gp_engine {
     st->max_stack_need = max_need;
     std::copy(op_count, op_count + GP_OP_COUNT, st->op_count);
     st->const_nodes = const_nodes;
+    st->const_programs = const_programs;
     if (best >= 0) {
       const float pen = cfg.parsimony * (float)pop[best].size();
       st->best_raw = fit[best];

@@ -37,9 +37,6 @@
 #ifndef GP_MINB
 #define GP_MINB 1   // minimum resident CTAs per SM (register budget = 64K / (GP_MINB * NT))
 #endif
-#ifndef GP_PREFETCH_CASE_ONLY
-#define GP_PREFETCH_CASE_ONLY 1   // 0: prefetch whole code words (more registers)
-#endif
 
 #define GP_CAT2(a, b) a##b
 #define GP_CAT(a, b) GP_CAT2(a, b)
@@ -61,10 +58,12 @@ static_assert(kStreamWin % 4 == 0, "stream window");
 constexpr float kLogLossLo = 1.0000000000000005e-15f;  // -ln(1 - 1e-15), S:191 clamp (C7)
 constexpr float kLogLossHi = 34.538776394910684f;      // -ln(1e-15)
 
-// Shared-memory layout (bytes): fp64 accumulators [NW][G][S] | ys[TILE] | ws[TILE] (weighted only)
-// | xs[n_cols][TILE] (small n_cols only) | code-stream window [kStreamWin + 2] uint4
+// Shared-memory layout (bytes): fp64 accumulators [NW][G][S] | reduction blocks [NW][kRedRows]
+// [kRedStride] fp32 | ys[TILE] | ws[TILE] (weighted only) | xs[n_cols][TILE] (small n_cols only)
+// | code-stream window [kStreamWin + 2] uint4
+static_assert(kRedBytes == NW * kRedRows * kRedStride * 4, "reduction block size");
 __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
-  return ((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15;
+  return (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15) + kRedBytes;
 }
 
 #define LBL(OPV, s) ((OPV) * kCaseStride + (s))
@@ -197,22 +196,6 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
   return v;
 }
 
-// Transposed butterfly: the warp sums of four per-lane values with 6 shuffles (instead of 4 x 5):
-// afterwards lane 0 holds sum(v0), lane 8 sum(v1), lane 16 sum(v2), lane 24 sum(v3).
-__device__ __forceinline__ float warp_sum4_f32(float v0, float v1, float v2, float v3, int lane) {
-  const bool lo16 = (lane & 16) == 0, lo8 = (lane & 8) == 0;
-  float k0 = lo16 ? v0 : v2, k1 = lo16 ? v1 : v3;
-  const float s0 = lo16 ? v2 : v0, s1 = lo16 ? v3 : v1;
-  k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
-  k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
-  float m = lo8 ? k0 : k1;
-  m += __shfl_xor_sync(0xffffffffu, lo8 ? k1 : k0, 8);
-  m += __shfl_xor_sync(0xffffffffu, m, 4);
-  m += __shfl_xor_sync(0xffffffffu, m, 2);
-  m += __shfl_xor_sync(0xffffffffu, m, 1);
-  return m;
-}
-
 template <bool PREDICT, bool XSMEM>
 // the global-X instantiation holds more live addresses: one resident CTA less
 __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB - 1 : 1))
@@ -225,6 +208,9 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
   const int n_groups = (count + a.G - 1) / a.G;
   const int64_t n_items = (int64_t)n_groups * a.n_chunks;
   double* acc = reinterpret_cast<double*>(smem);                 // [NW][G][S]
+  // this warp's transposed reduction block [kRedRows][kRedStride] (single-sum metrics)
+  float* rbw = reinterpret_cast<float*>(smem + (PREDICT ? 0 : smem_acc_bytes(a.G, S) - kRedBytes)) +
+               warp * (kRedRows * kRedStride);
   const bool has_w = a.w != nullptr;
   // global-X path: 16-byte vector loads when every column start is 16-byte aligned
   const bool x_vec = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && ((a.ldx & 3) == 0);
@@ -274,35 +260,41 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
       // ---- A3 + A4 + A5: walk the group's code stream --------------------------------------
       int ebase = tid * 4;                           // element e(r) = ebase + (r/4)*NT*4 + r%4
       float l0 = 0.f, l1 = 0.f, l2 = 0.f;
-      // single-sum metrics: per-lane sums of up to three finished programs wait here so four
-      // programs share one transposed warp reduction (warp_sum4_f32)
-      float pend0 = 0.f, pend1 = 0.f, pend2 = 0.f;
-      int pidx0 = 0, pidx1 = 0, pidx2 = 0, npend = 0;
-      auto reduce4 = [&](float v3, int i3, int n) {   // n programs valid (1..4)
-        const float m = warp_sum4_f32(pend0, pend1, pend2, v3, lane);
-        const int j = lane >> 3;
-        if ((lane & 7) == 0 && j < n) {
-          const int pl = j == 0 ? pidx0 : j == 1 ? pidx1 : j == 2 ? pidx2 : i3;
-          acc[(size_t)warp * a.G + pl] += (double)m;
-        }
+      // unweighted MSE / RMSE over a full tile: the FFMA-only loss, chosen once per tile
+      const bool fast_mse = !PREDICT && (a.metric == GP_MSE || a.metric == GP_RMSE) && !has_w &&
+                            nvalid == TILE;
+      // Single-sum metrics (A5): each lane stores its fp32 sum of a finished program into row
+      // (slot % kRedRows) of the warp's block; every kRedRows programs the warp reduces the
+      // block at once -- lane L sums half a row (4 LDS.128), one shuffle joins the halves, and
+      // the even lanes add the kRedRows program sums into their fp64 accumulators. Fixed order
+      // -> deterministic. (Replaces one shuffle butterfly per program.)
+      auto flush = [&](int p0, int n) {
+        __syncwarp();
+        const int row = lane >> 1, half = lane & 1;
+        const float4* src = reinterpret_cast<const float4*>(rbw + row * kRedStride + half * 16);
+        const float4 v0 = src[0], v1 = src[1], v2 = src[2], v3 = src[3];
+        float m = ((v0.x + v0.y) + (v0.z + v0.w)) + ((v1.x + v1.y) + (v1.z + v1.w)) +
+                  (((v2.x + v2.y) + (v2.z + v2.w)) + ((v3.x + v3.y) + (v3.z + v3.w)));
+        m += __shfl_xor_sync(0xffffffffu, m, 1);
+        if (half == 0 && row < n) acc[(size_t)warp * a.G + p0 + row] += (double)m;
+        __syncwarp();
       };
       float st[STACK][R];
       // fused weighted loss of the current pass's rows (A4)
+      // unweighted full tile: every row is live, w = 1 (FP32x2 sub + FFMA2 only)
+      auto loss_fast_mse = [&]() {
+#pragma unroll
+        for (int k = 0; k < R4; ++k) {
+          const float4 yv = *reinterpret_cast<const float4*>(ys + ebase + k * NT * 4);
+          float d0, d1, d2, d3;
+          sub_x2(d0, d1, st[0][4 * k], st[0][4 * k + 1], yv.x, yv.y);
+          sub_x2(d2, d3, st[0][4 * k + 2], st[0][4 * k + 3], yv.z, yv.w);
+          fma_x2(l0, l1, d0, d1, d0, d1, l0, l1);  // even / odd rows: l1 joins l0 at the end
+          fma_x2(l0, l1, d2, d3, d2, d3, l0, l1);
+        }
+      };
       auto loss = [&](auto tag, float Kp) {
         constexpr int M = decltype(tag)::value;
-        if (M == GP_MSE && !has_w && nvalid == TILE) {
-          // unweighted full tile: every row is live, w = 1
-#pragma unroll
-          for (int k = 0; k < R4; ++k) {
-            const float4 yv = *reinterpret_cast<const float4*>(ys + ebase + k * NT * 4);
-            float d0, d1, d2, d3;
-            sub_x2(d0, d1, st[0][4 * k], st[0][4 * k + 1], yv.x, yv.y);
-            sub_x2(d2, d3, st[0][4 * k + 2], st[0][4 * k + 3], yv.z, yv.w);
-            fma_x2(l0, l1, d0, d1, d0, d1, l0, l1);  // even / odd rows: l1 joins l0 at the end
-            fma_x2(l0, l1, d2, d3, d2, d3, l0, l1);
-          }
-          return;
-        }
 #pragma unroll
         for (int k = 0; k < R4; ++k) {
           const float4 yv = *reinterpret_cast<const float4*>(ys + ebase + k * NT * 4);
@@ -349,6 +341,8 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
             const int e = ebase + (r >> 2) * NT * 4 + (r & 3);
             if (e < nvalid) o[e] = st[0][r];
           }
+        } else if (fast_mse) {
+          loss_fast_mse();
         } else {
           switch (a.metric) {
             case GP_MAE: loss(MTag<GP_MAE>{}, 0.0f); break;
@@ -368,68 +362,51 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
           for (int i = tid; i < wn + 2; i += NT) sw[i] = __ldg(a.stream + s_begin + w0 + i);
           __syncthreads();
         }
-#if GP_PREFETCH_CASE_ONLY
         // prefetch only the case ids (2 registers); the payload word is read from the window
-        // at the top of each iteration (its LDS latency overlaps the dispatch branch)
-        uint32_t c_n = sw[0].x, c_n2 = sw[1].x;
-#else
-        uint4 nxt = sw[0], nxt2 = sw[1];
-#endif
+        // at the top of each iteration (its LDS latency overlaps the dispatch branch). The loop
+        // has no trip counter: the window's last word carries kEndWin (pack_kernel).
+        const uint4* wp = sw;
+        uint32_t c_n = wp[0].x, c_n2 = wp[1].x;
 #pragma unroll 1
-        for (int kk = 0; kk < wn; ++kk) {
-#if GP_PREFETCH_CASE_ONLY
+        for (;;) {
           const uint32_t cid = c_n;
           c_n = c_n2;
-          c_n2 = sw[kk + 2].x;                       // window carries two look-ahead words
-          const uint4 cw = sw[kk];
-#else
-          const uint4 cw = nxt;
-          nxt = nxt2;
-          nxt2 = sw[kk + 2];                         // window carries two look-ahead words
-          const uint32_t cid = cw.x;
-#endif
-          switch (cid >> 2) {                        // case id * 4 (jump-table offset)
+          c_n2 = wp[2].x;                            // window carries two look-ahead words
+          const uint4 cw = *wp;
+          ++wp;
+          switch (cid) {                             // one jump table (BRX) over every case
             GP_ALL_CASES
             default: __builtin_unreachable();        // stage / pack guarantee a valid case
           }
-          if (cw.w) {                                // last word of a row pass (pack_kernel)
-            end_pass();
-            if (cw.w & kEndPass) {                   // next row pass of the same program
-              ebase = (int)(cw.w >> 8) * NT * R + tid * 4;
-            } else {                                 // program done: warp-reduce into smem (A5)
-              if constexpr (!PREDICT) {
-                const int j = (int)(cw.w >> 8);      // == pslot
-                if (S == 1) {
-                  const float lp = l0 + l1;          // l1: odd rows of the paired MSE path
-                  if (npend == 3) {                  // fourth program: one batched reduction
-                    reduce4(lp, j, 4);
-                    npend = 0;
+          if (cw.w) {                                // last word of a row pass or of the window
+            if (cw.w & (kEndPass | kEndProgram)) {
+              end_pass();
+              if (cw.w & kEndPass) {                 // next row pass of the same program
+                ebase = (int)(cw.w >> 8) * NT * R + tid * 4;
+              } else {                               // program done (A5)
+                if constexpr (!PREDICT) {
+                  const int j = (int)(cw.w >> 8);    // == pslot
+                  if (S == 1) {
+                    rbw[(j % kRedRows) * kRedStride + lane] = l0 + l1;  // l1: odd rows (MSE)
+                    if (j % kRedRows == kRedRows - 1) flush(j - (kRedRows - 1), kRedRows);
                   } else {
-                    pend0 = pend1; pend1 = pend2; pend2 = lp;
-                    pidx0 = pidx1; pidx1 = pidx2; pidx2 = j;
-                    ++npend;
+                    double* slot = acc + ((size_t)warp * a.G + j) * S;
+                    const double v0 = warp_sum_f64(l0), v1 = warp_sum_f64(l1),
+                                 v2 = warp_sum_f64(l2);
+                    if (lane == 0) { slot[0] += v0; slot[1] += v1; slot[2] += v2; }
                   }
-                } else {
-                  double* slot = acc + ((size_t)warp * a.G + j) * S;
-                  const double v0 = warp_sum_f64(l0), v1 = warp_sum_f64(l1), v2 = warp_sum_f64(l2);
-                  if (lane == 0) { slot[0] += v0; slot[1] += v1; slot[2] += v2; }
+                  l0 = l1 = l2 = 0.f;
                 }
-                l0 = l1 = l2 = 0.f;
+                ebase = tid * 4;
+                ++pslot;
               }
-              ebase = tid * 4;
-              ++pslot;
             }
+            if (cw.w & kEndWin) break;
           }
         }
       }
-      if (!PREDICT && S == 1 && npend > 0) {         // leftover batch at the end of the tile
-        // pending programs sit in the LAST npend slots of (pend0, pend1, pend2)
-        const int n = npend;
-        if (n == 1) { pend0 = pend2; pidx0 = pidx2; pend1 = pend2 = 0.f; }
-        else if (n == 2) { pend0 = pend1; pidx0 = pidx1; pend1 = pend2; pidx1 = pidx2; pend2 = 0.f; }
-        reduce4(0.f, 0, n);
-        npend = 0;
-      }
+      if (!PREDICT && S == 1 && np % kRedRows != 0)  // last partial block of the tile
+        flush(np - np % kRedRows, np % kRedRows);
     }
 
     if constexpr (!PREDICT) {

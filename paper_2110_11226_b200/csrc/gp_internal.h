@@ -49,6 +49,7 @@ struct gp_context {
   int64_t prof_launches = 0;
   int64_t kernel_launches = 0;   // gp_context_kernel_launches
   bool sethi_ullman = true;      // gp_context_set_eval_order
+  bool const_programs = true;    // gp_context_set_const_programs (closed-form constant programs)
 
   std::vector<gpb::StageBuf*> all_buffers() {
     return {&code, &code_off, &code_len, &need, &lists, &pos, &gstart, &counts, &codestream, &scratch, &status,

@@ -19,10 +19,17 @@ constexpr int kVariantStack[kNumVariants] = {4, 8, 12, 20};
 
 // Pass flags in .w of the LAST code word of each row pass of a program in a code stream:
 // bits 0-1 = kEndPass (another pass follows; bits 8.. = its index) or kEndProgram (bits 8.. =
-// the program's slot in its group).
-constexpr uint32_t kEndPass = 1u, kEndProgram = 2u;
+// the program's slot in its group). kEndWin (bit 2) marks the last word of a shared-memory
+// stream window (every kStreamWin-th word of a group's stream, and its last word), so the
+// evaluator's word loop needs no trip counter.
+constexpr uint32_t kEndPass = 1u, kEndProgram = 2u, kEndWin = 4u;
 // Code-stream window staged in shared memory per CTA (words of 16 B).
 constexpr int kStreamWin = 768;
+// Per-warp transposed reduction block of the single-sum metrics (eval_impl.cuh): kRedRows
+// programs x 32 lanes of fp32 per-lane sums, rows padded to kRedStride floats so the
+// row-half LDS.128 reads of a warp hit 32 distinct banks.
+constexpr int kRedRows = 16, kRedStride = 36;
+constexpr int kRedBytes = 4 * kRedRows * kRedStride * 4;  // 4 warps per CTA (NT = 128)
 
 // Everything the fused evaluator needs for one launch (see eval_impl.cuh). Each variant runs a
 // packed CODE STREAM per program group: for every program of the group, SUB copies of its code

@@ -339,3 +339,46 @@ def test_single_rank_nccl_context_matches(gp, ctx):
         assert torch.equal(a, b) and torch.equal(sa, sb)
     assert c1.kernel_launches() > 0
     c1.close()
+
+
+# ---- variable-free programs (closed-form fitness, gp_context_set_const_programs) ---------------
+def _constant_heavy_population(n, seed):
+    """Random programs where every other one has its variables replaced by constants: lone
+    constants and variable-free trees of every depth, mixed with ordinary programs."""
+    nodes, off = synth.random_population(n, seed=seed, depth=(0, 5), n_features=2, max_stack=8)
+    nodes = nodes.copy()
+    rng = np.random.default_rng(seed)
+    for p in range(0, n, 2):
+        seg = nodes[off[p]:off[p + 1]]         # (len, 2) int32 view: opcode, var / f32 bits
+        var = seg[:, 0] == synth.VAR
+        seg[var, 1] = rng.uniform(-1.5, 1.5, int(var.sum())).astype(np.float32).view(np.int32)
+        seg[var, 0] = synth.CONST
+    return nodes, off
+
+
+@pytest.mark.parametrize("metric", ["mse", "rmse", "pearson", "mae", "logloss"])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_constant_programs_match_oracle(gp, ctx, orc, metric, weighted):
+    """Variable-free programs skip the per-row evaluator for MSE / RMSE / Pearson (closed form
+    from W, S_y, S_yy); every metric must still match the oracle, and the closed form must
+    agree with the per-row evaluation of the same programs."""
+    n_rows = 2 * 2048 + 999
+    X, y = _dataset(metric, n_rows, seed=8)
+    nodes, off = _constant_heavy_population(200, seed=31)
+    w = synth.weights(n_rows, seed=6) if weighted else None
+    args = (dev(nodes), dev(off), dev(X), dev(y), None if w is None else dev(w))
+    fit, st = ctx.evaluate(*args, metric=metric, max_stack=8)
+    ctx.set_const_programs(False)
+    try:
+        fit_rows, st_rows = ctx.evaluate(*args, metric=metric, max_stack=8)
+    finally:
+        ctx.set_const_programs(True)
+    torch.cuda.synchronize()
+    ref, sens, flags = orc.population_fitness(nodes, off, X, y, w, metric)
+    check_fitness(fit.cpu().numpy(), ref, sens, flags, metric)
+    check_fitness(fit_rows.cpu().numpy(), ref, sens, flags, metric)
+    assert np.array_equal(st.cpu().numpy(), st_rows.cpu().numpy())
+    a, b = fit.cpu().numpy(), fit_rows.cpu().numpy()
+    fin = np.isfinite(a) & np.isfinite(b)
+    assert np.array_equal(np.isfinite(a), np.isfinite(b))
+    assert np.all(np.abs(a[fin] - b[fin]) <= 1e-5 * np.maximum(np.abs(b[fin]), 1e-6))
