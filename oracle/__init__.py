@@ -34,7 +34,7 @@ N_OPS = 26
 NAMES = ["var", "const", "add", "sub", "mul", "div", "min", "max", "pow", "sin", "cos", "tan",
          "abs", "neg", "sqrt", "log", "exp", "inv", "square", "cube", "tanh", "sinh", "cosh",
          "asin", "acos", "atan"]
-METRICS = {"mae": 0, "mse": 1, "rmse": 2, "logloss": 3, "pearson": 4}
+METRICS = {"mae": 0, "mse": 1, "rmse": 2, "logloss": 3, "pearson": 4, "spearman": 5}
 # Program flags returned by population_fitness.
 F_OVERFLOW, F_AMBIGUOUS, F_INVALID, F_UNDEFINED = 1, 2, 4, 8
 
@@ -68,6 +68,7 @@ def lib():
         L.orc_eval_program.restype = None
         L.orc_eval_row.argtypes, L.orc_eval_row.restype = [P, P, i64, i64], dbl
         L.orc_fitness.argtypes, L.orc_fitness.restype = [ctypes.c_int, P, P, P, i64, P], dbl
+        L.orc_rank_vector.argtypes, L.orc_rank_vector.restype = [P, i64, P], None
         L.orc_fitness_sensitivity.argtypes = [ctypes.c_int, P, P, P, P, i64]
         L.orc_fitness_sensitivity.restype = dbl
         L.orc_philox4x32_10.argtypes, L.orc_philox4x32_10.restype = [P, P, P], None
@@ -179,6 +180,14 @@ def fitness(metric, yhat, y, w=None):
     und = ctypes.c_int(0)
     f = lib().orc_fitness(m, _p(yh), _p(yy), _p(ww), len(yh), ctypes.byref(und))
     return f, bool(und.value)
+
+
+def rank_vector(values):
+    """ranks 1..n, ties averaged."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    out = np.empty(len(v), np.float64)
+    lib().orc_rank_vector(_p(v), len(v), _p(out))
+    return out
 
 
 def fitness_sensitivity(metric, yhat, err, y, w=None) -> float:

@@ -22,6 +22,9 @@
  *   - weighted metrics MAE/MSE/RMSE/LogLoss/Pearson (two-pass)
  *                                                        SPEC examples, closed forms on Pagie grids,
  *                                                        identities (RMSE^2 = MSE, Pearson(y,y)=1 ...)
+ *   - rank_vector (average ties) and Spearman = weighted Pearson of ranks   P:274-277; S:201,
+ *     S:209-215, S:219-220                               SPEC examples, scipy rankdata / spearmanr,
+ *                                                        monotone-transform invariance
  *   - Philox4x32-10                                      P:202 (Salmon et al. 2011)   Random123 KATs
  *   - tournament selection with parsimony (Eqs. 1-2)
  *                                                        brute force on tiny populations, closed-form
@@ -318,9 +321,89 @@ static double row_loss(int metric, double y, double yh) {
   return NAN;
 }
 
+/* rank_vector: ranks 1..n ascending, ties get the average of the positions they cover
+ * ("average-tie rule"). Sorting is a library step (qsort); ties are then averaged per run. */
+typedef struct { double v; int64_t i; } vidx;
+static int cmp_vidx(const void* a, const void* b) {
+  const double x = ((const vidx*)a)->v, y = ((const vidx*)b)->v;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+void orc_rank_vector(const double* v, int64_t n, double* ranks) {
+  vidx* t = (vidx*)malloc(sizeof(vidx) * (size_t)(n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) { t[i].v = v[i]; t[i].i = i; }
+  qsort(t, (size_t)n, sizeof(vidx), cmp_vidx);
+  for (int64_t s = 0; s < n;) {
+    int64_t e = s + 1;
+    while (e < n && t[e].v == t[s].v) ++e;
+    const double r = 0.5 * (double)(s + 1 + e);   /* average of positions s+1 .. e */
+    for (int64_t k = s; k < e; ++k) ranks[t[k].i] = r;
+    s = e;
+  }
+  free(t);
+}
+
+/* weighted Pearson correlation of a and b: weighted means first, then centred sums
+ * (two-pass); w == 0 rows skipped; zero variance or non-finite r -> 0 and *undefined = 1. */
+static double pearson_w(const double* a, const double* b, const float* w, int64_t n, double W,
+                        int* undefined) {
+  double ma = 0.0, mb = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double wi = w ? (double)w[i] : 1.0;
+    if (wi == 0.0) continue;
+    ma += wi * a[i];
+    mb += wi * b[i];
+  }
+  ma /= W;
+  mb /= W;
+  double sab = 0.0, saa = 0.0, sbb = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double wi = w ? (double)w[i] : 1.0;
+    if (wi == 0.0) continue;
+    double da = a[i] - ma, db = b[i] - mb;
+    sab += wi * da * db;
+    saa += wi * da * da;
+    sbb += wi * db * db;
+  }
+  double r = sab / sqrt(saa * sbb);
+  if (!isfinite(r) || !(saa > 0.0) || !(sbb > 0.0)) {
+    if (undefined) *undefined = 1;
+    return 0.0;
+  }
+  return r;
+}
+
 double orc_fitness(int metric, const double* yh, const float* y, const float* w, int64_t n,
                    int* undefined) {
   if (undefined) *undefined = 0;
+  if (metric == 5) {
+    /* Spearman: Pearson of rank_vector(y) and rank_vector(yhat) with the same weights.
+     * The ranks are taken over every row (rank_vector has no weights). Reading: the predictions
+     * are ranked at the evaluator's precision (fp32: where floating point decides an integer,
+     * both sides decide in the kernel's precision); non-finite predictions leave the ranks
+     * undefined (S:210 pre: finite values) -> 0 and *undefined = 1, as for Pearson. */
+    double W = 0.0;
+    for (int64_t i = 0; i < n; ++i) W += w ? (double)w[i] : 1.0;
+    double* a = (double*)malloc(sizeof(double) * (size_t)n);
+    double* b = (double*)malloc(sizeof(double) * (size_t)n);
+    double* ra = (double*)malloc(sizeof(double) * (size_t)n);
+    double* rb = (double*)malloc(sizeof(double) * (size_t)n);
+    int finite = 1;
+    for (int64_t i = 0; i < n; ++i) {
+      a[i] = (double)(float)yh[i];
+      b[i] = (double)y[i];
+      if (!isfinite(a[i])) finite = 0;
+    }
+    double r = 0.0;
+    if (!finite) {
+      if (undefined) *undefined = 1;
+    } else {
+      orc_rank_vector(a, n, ra);
+      orc_rank_vector(b, n, rb);
+      r = pearson_w(ra, rb, w, n, W, undefined);
+    }
+    free(a); free(b); free(ra); free(rb);
+    return r;
+  }
   double W = 0.0;
   for (int64_t i = 0; i < n; ++i) W += w ? (double)w[i] : 1.0;
   if (metric <= 3) {
@@ -389,6 +472,9 @@ double orc_fitness_sensitivity(int metric, const double* yh, const double* E, co
     }
     return s;
   }
+  /* Spearman: ranks change by whole steps, no first-order bound (tests use exactly representable
+   * inputs or a rank-swap tolerance) */
+  if (metric == 5) return 0.0;
   /* Pearson: |dr/dyh_i| = w_i |(y_i - my)/sqrt(sxx syy) - r (yh_i - mh)/sxx| */
   double my = 0.0, mh = 0.0;
   for (int64_t i = 0; i < n; ++i) {
@@ -508,7 +594,7 @@ void orc_population_fitness(const onode* nodes, const int64_t* offsets, int32_t 
     int64_t len = offsets[p + 1] - offsets[p];
     int32_t flags = 0;
     if (orc_validate(prog, len, n_cols) != 0) {
-      out_fitness[p] = metric == 4 ? -INFINITY : INFINITY;
+      out_fitness[p] = metric >= 4 ? -INFINITY : INFINITY;
       if (out_sens) out_sens[p] = 0.0;
       if (out_flags) out_flags[p] = 4;
       continue;

@@ -106,3 +106,60 @@ def test_logloss_clamp(orc):
     # S:191 clamp: p in [1e-15, 1 - 1e-15] -> per-row loss <= -ln(1e-15)
     assert F(orc, "logloss", [-1e4], [1.0]) == pytest.approx(-math.log(1e-15), rel=1e-12)
     assert F(orc, "logloss", [1e4], [1.0]) == pytest.approx(-math.log1p(-1e-15), rel=1e-6)
+
+
+# ---- Spearman -------------------------------------------
+def test_rank_vector_spec_examples(orc):
+    assert orc.rank_vector([10, 30, 20]).tolist() == [1, 3, 2]
+    assert orc.rank_vector([5, 5]).tolist() == [1.5, 1.5]
+    assert orc.rank_vector([2, 1, 2, 3]).tolist() == [2.5, 1, 2.5, 4]
+
+
+def test_rank_vector_matches_scipy(orc):
+    from scipy.stats import rankdata
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 7, 100, 1000):
+        v = rng.integers(-5, 6, n).astype(np.float64)                   # many ties
+        assert np.array_equal(orc.rank_vector(v), rankdata(v, method="average"))
+        u = rng.standard_normal(n)
+        assert np.array_equal(orc.rank_vector(u), rankdata(u, method="average"))
+
+
+def test_spearman_matches_scipy_unweighted(orc):
+    from scipy.stats import spearmanr
+    rng = np.random.default_rng(4)
+    for n in (5, 50, 2000):
+        y = rng.integers(0, 20, n).astype(np.float32)
+        yh = (rng.integers(0, 30, n) + 0.5 * y).astype(np.float64)      # fp32-exact, with ties
+        f, und = orc.fitness("spearman", yh, y)
+        assert not und
+        assert abs(f - spearmanr(yh, y).statistic) <= 1e-12
+
+
+def test_spearman_weighted_is_pearson_of_ranks(orc):
+    """S:219 identity with weights, against numpy's weighted covariance on scipy ranks."""
+    from scipy.stats import rankdata
+    rng = np.random.default_rng(5)
+    n = 777
+    y = rng.standard_normal(n).astype(np.float32)
+    yh = np.round(rng.standard_normal(n) * 8).astype(np.float64)
+    w = synth.weights(n, seed=2)
+    c = np.cov(rankdata(yh), rankdata(y), aweights=w)
+    ref = c[0, 1] / math.sqrt(c[0, 0] * c[1, 1])
+    f, und = orc.fitness("spearman", yh, y, w)
+    assert not und and abs(f - ref) <= 1e-12
+
+
+def test_spearman_monotone_invariance_and_special_cases(orc):
+    rng = np.random.default_rng(6)
+    y = rng.integers(0, 50, 500).astype(np.float32)
+    yh = rng.integers(-20, 20, 500).astype(np.float64)
+    f0, _ = orc.fitness("spearman", yh, y)
+    for g in (lambda v: 3 * v + 1, lambda v: v ** 3, lambda v: np.exp(v / 8)):
+        assert orc.fitness("spearman", g(yh), y)[0] == pytest.approx(f0, abs=1e-12)   # S:220
+    assert orc.fitness("spearman", y.astype(np.float64), y)[0] == pytest.approx(1.0, abs=1e-12)
+    assert orc.fitness("spearman", -y.astype(np.float64), y)[0] == pytest.approx(-1.0, abs=1e-12)
+    assert orc.fitness("spearman", np.full(500, 2.0), y) == (0.0, True)          # constant
+    bad = yh.copy()
+    bad[3] = np.nan
+    assert orc.fitness("spearman", bad, y) == (0.0, True)                         # non-finite
