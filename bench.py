@@ -118,7 +118,7 @@ class ClockSampler:
 
 # metrics whose variable-free programs get their fitness from the dataset moments (no per-row
 # loss; gp_context_set_const_programs)
-CLOSED_FORM_METRICS = ("mse", "rmse", "pearson")
+CLOSED_FORM_METRICS = ("mse", "rmse", "logloss", "pearson")
 
 
 def algorithmic_ops(op_count, rows, metric, n_programs, const_programs=0):
@@ -205,7 +205,10 @@ def run_b200(args, cfg):
     stream = torch.cuda.Stream(local)
     ctx = gp.Context(local, stream=stream, unique_id=uid, rank=rank, world_size=world)
     ctx.set_const_programs(not args.no_const_programs)
-    Xh, yh, x0, y0, m_global = load_dataset(cfg, rank, world)
+    by_prog = args.shard == "programs"
+    if by_prog:                                   # all rows on every rank
+        ctx.set_shard("programs")
+    Xh, yh, x0, y0, m_global = load_dataset(cfg, 0 if by_prog else rank, 1 if by_prog else world)
     ctx.set_reference_row(x0, y0)
     X = torch.from_numpy(Xh).cuda(local)
     y = torch.from_numpy(yh).cuda(local)
@@ -251,7 +254,9 @@ def run_b200(args, cfg):
 
     # roofline of the dominant kernel (the fused evaluator), this rank's launches: algorithmic
     # per-row work = variable-dependent nodes only (variable-free subtrees are constants)
-    rows_local = X.shape[1]
+    # this rank's share of the per-row work: its row shard, or (program sharding) all rows x about
+    # 1 / world of the programs
+    rows_local = X.shape[1] / (world if by_prog else 1)
     sfu = fp32 = 0
     for s in steps:
         a, b2 = algorithmic_ops(s["op_count"], rows_local, cfg["metric"], cfg["pop"],
@@ -338,7 +343,8 @@ def run_b200(args, cfg):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, DESIGN.md recipe)",
             "config": {"workload": cfg["workload"], "rows": m_global, "population": cfg["pop"],
                        "metric": cfg["metric"], "mean_program_length": round(mean_len, 3),
-                       "parallelism": f"rows sharded over {world} GPU(s)",
+                       "parallelism": (f"programs sharded over {world} GPU(s), fitness all-gathered"
+                                       if by_prog else f"rows sharded over {world} GPU(s)"),
                        "l2": "inputs larger than L2 (X + y = %.0f MB)" % ((Xh.nbytes + yh.nbytes) * world / 1e6)},
             "roofline": roofline, "roofline_gen0": roof0,
             "var_node_evals_per_s": var_nodes / (ms * 1e-3), "const_node_share": round(const_share, 4),
@@ -412,6 +418,9 @@ def main():
     ap.add_argument("--weak", action="store_true", help="per-GPU rows fixed (default: strong)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="rows", choices=["rows", "programs"],
+                    help="multi-GPU split: row shards + partial-sum all-reduce (default) or "
+                         "program chunks + fitness all-gather (SURVEY F3)")
     ap.add_argument("--no-const-programs", action="store_true",
                     help="evaluate variable-free programs per row (no closed-form fitness)")
     ap.add_argument("--dump-population", default=None,

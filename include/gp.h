@@ -37,15 +37,18 @@ typedef enum {
   GP_OK = 0,
   GP_ERR_ARG = 1,          /* invalid argument (sizes, pointers, metric, config) */
   GP_ERR_PROGRAM = 2,      /* reserved: per-program errors are reported via status bits */
-  GP_ERR_UNSUPPORTED = 3,  /* e.g. Spearman fitness, world_size > 1 without NCCL */
+  GP_ERR_UNSUPPORTED = 3,  /* e.g. Spearman with row-sharded ranks, world_size > 1 without NCCL */
   GP_ERR_CUDA = 4,         /* a CUDA runtime call failed; see gp_last_error */
   GP_ERR_NCCL = 5,         /* an NCCL call failed or libnccl could not be loaded */
   GP_ERR_OOM = 6           /* device allocation failed */
 } gp_status;
 
 /* Fitness metrics, P:264-275 ("weighted versions of the following 6 standard loss functions").
- * MAE, MSE, RMSE, LogLoss: lower is better. Pearson: higher is better.
- * Spearman is defined by the paper but is not on this hot path: GP_ERR_UNSUPPORTED. */
+ * MAE, MSE, RMSE, LogLoss: lower is better. Pearson, Spearman: higher is better.
+ * Spearman = weighted Pearson of rank_vector(y) and rank_vector(yhat), ranks
+ * 1..n over every row with ties averaged, yhat ranked in fp32. It cannot stream: its
+ * gp_evaluate path materialises yhat per batch of programs and sorts it; with a
+ * row-sharded multi-rank context it returns GP_ERR_UNSUPPORTED (use GP_SHARD_PROGRAMS). */
 typedef enum {
   GP_MAE = 0, GP_MSE = 1, GP_RMSE = 2, GP_LOGLOSS = 3, GP_PEARSON = 4, GP_SPEARMAN = 5
 } gp_metric;
@@ -143,12 +146,22 @@ gp_status gp_context_set_eval_order(gp_context* ctx, int sethi_ullman);
 /* Variable-free programs: a program whose whole tree folds to one constant c at compile time
  * (stage kernel) predicts c on every row. With closed_form = 1 (default) gp_evaluate takes its
  * MSE / RMSE sum from the dataset moments, sum_i w_i (c - y_i)^2 = W c^2 - 2 c S_y + S_yy
- * (fp64, the same per-chunk W, S_y, S_yy the Pearson path uses), and reports its Pearson
- * correlation as undefined (0, GP_FLAG_UNDEFINED_CORR) -- both without a per-row pass. This is
- * the per-row loss of P:256-262 with the constant prediction factored out of the sum. MAE and
- * LogLoss still evaluate such programs per row. 0: every program goes through the per-row
- * evaluator. */
+ * (fp64, the same per-chunk W, S_y, S_yy the Pearson path uses), its LogLoss sum from the two
+ * per-row values it can take, W_1 softplus(-c) + (W - W_1) softplus(c) (W_1 = weight of rows with
+ * y > 1/2, clamped as in S:191), and reports its Pearson correlation as undefined (0,
+ * GP_FLAG_UNDEFINED_CORR) -- all without a per-row pass. This is the per-row loss of P:256-262
+ * with the constant prediction factored out of the sum. MAE still evaluates such programs per
+ * row. 0: every program goes through the per-row evaluator. */
 gp_status gp_context_set_const_programs(gp_context* ctx, int closed_form);
+/* Multi-GPU work split of gp_evaluate on a context with world > 1.
+ *  GP_SHARD_ROWS (default): each rank passes its contiguous row shard; the per-program fp64
+ *    partial sums are combined by one ncclAllReduce before finalize.
+ *  GP_SHARD_PROGRAMS: each rank passes ALL rows and evaluates the programs [r c, min(n, (r+1) c))
+ *    with c = ceil(n / world); the fp32 fitness and status words of the chunks are combined by
+ *    ncclAllGather (in place, padded to world x c). Suits small datasets with large populations.
+ * Results are identical on every rank in both modes. */
+typedef enum { GP_SHARD_ROWS = 0, GP_SHARD_PROGRAMS = 1 } gp_shard;
+gp_status gp_context_set_shard(gp_context* ctx, gp_shard mode);
 /* Number of CUDA kernels this context has launched (all entry points) since the last reset. */
 gp_status gp_context_kernel_launches(gp_context* ctx, int64_t* launches, int reset);
 

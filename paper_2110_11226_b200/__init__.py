@@ -126,6 +126,13 @@ class Context:
                                             int(reset)), self.handle, "eval_timing")
         return ms.value, n.value
 
+    def set_shard(self, mode: str = "rows"):
+        """gp_context_set_shard: "rows" (each rank passes its row shard; partial sums all-reduced)
+        or "programs" (each rank passes all rows, evaluates its program chunk; fitness
+        all-gathered)."""
+        _check(lib().gp_context_set_shard(self.handle, {"rows": 0, "programs": 1}[mode]),
+               self.handle, "set_shard")
+
     def set_const_programs(self, closed_form: bool = True):
         """gp_context_set_const_programs: variable-free programs' MSE / RMSE / Pearson fitness from
         the dataset moments (default) or through the per-row evaluator."""

@@ -29,6 +29,7 @@ SIGNATURES = {
     "gp_context_kernel_launches": ([P, ctypes.POINTER(i64), ctypes.c_int], ctypes.c_int),
     "gp_context_set_eval_order": ([P, ctypes.c_int], ctypes.c_int),
     "gp_context_set_const_programs": ([P, ctypes.c_int], ctypes.c_int),
+    "gp_context_set_shard": ([P, ctypes.c_int], ctypes.c_int),
     "gp_evaluate": ([P, P, P, i32, i64, i32, P, i64, P, P, i64, i32, ctypes.c_int, P, P],
                     ctypes.c_int),
     "gp_predict": ([P, P, P, i32, i64, i32, P, i64, i64, i32, P, i64, P], ctypes.c_int),

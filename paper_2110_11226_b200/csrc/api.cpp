@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -26,6 +27,8 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi& nccl() {
@@ -39,8 +42,10 @@ NcclApi& nccl() {
       api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
       api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
       api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
       api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce;
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce &&
+               api.AllGather;
     }
   }
   return api;
@@ -121,7 +126,6 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   EvalPlan pl;
   const int tile = kTile;
   const int64_t n_tiles = (n_rows + tile - 1) / tile;
-  const int NW = 4;  // NT = 128 in every variant
   const int g_max = 128;
   pl.xsmem = (size_t)n_cols * tile * sizeof(float) <= 96 * 1024;
   const int occ_guess = 4;
@@ -136,10 +140,9 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   pl.n_groups = n_groups;
   pl.n_chunks = Q;
   pl.rows_per_chunk = tpc * tile;
-  const size_t acc = predict ? 0 : (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15) +
-                                    (size_t)kRedBytes;
   const size_t yw = predict ? 0 : (weighted ? 2 : 1) * (size_t)tile * sizeof(float);
-  pl.smem = acc + yw + (pl.xsmem ? (size_t)n_cols * tile * sizeof(float) : 0) +
+  // tiles + stream window; each variant adds its accumulator / reduction block bytes at launch
+  pl.smem = yw + (pl.xsmem ? (size_t)n_cols * tile * sizeof(float) : 0) +
             (size_t)(kStreamWin + 2) * 16;
   return pl;
 }
@@ -172,8 +175,9 @@ static gp_status launch_variants(gp_context* ctx, EvalArgs a, const EvalPlan& pl
     a.prog_ids = (const int32_t*)ctx->lists.p + (int64_t)v * n;
     a.prog_count = (const int32_t*)ctx->counts.p + v;
     a.work_counter = (int32_t*)ctx->counts.p + kNumVariants + v;
-    const int occ = std::max(1, var.occupancy(predict, pl.xsmem, pl.smem));
-    gp_status s = ctx->launch(var.launch(a, predict, pl.xsmem, ctx->sms * occ, pl.smem, ctx->stream),
+    const size_t smem = pl.smem + (predict ? 0 : var.acc_bytes(pl.G, a.metric == GP_PEARSON ? 3 : 1));
+    const int occ = std::max(1, var.occupancy(predict, pl.xsmem, smem));
+    gp_status s = ctx->launch(var.launch(a, predict, pl.xsmem, ctx->sms * occ, smem, ctx->stream),
                             predict ? "predict kernel" : "eval kernel");
     if (s) return s;
   }
@@ -292,6 +296,12 @@ gp_status gp_context_eval_timing(gp_context* ctx, double* total_ms, int64_t* lau
   return GP_OK;
 }
 
+gp_status gp_context_set_shard(gp_context* ctx, gp_shard mode) {
+  if (!ctx || (mode != GP_SHARD_ROWS && mode != GP_SHARD_PROGRAMS)) return GP_ERR_ARG;
+  ctx->shard = mode;
+  return GP_OK;
+}
+
 gp_status gp_context_set_const_programs(gp_context* ctx, int closed_form) {
   if (!ctx) return GP_ERR_ARG;
   ctx->const_programs = closed_form != 0;
@@ -325,12 +335,16 @@ gp_status gp_context_set_reference_row(gp_context* ctx, const float* x_ref, int3
   return ctx->cuda(cudaStreamSynchronize(ctx->stream), "xref sync");
 }
 
+static gp_status bucket_pack(gp_context* ctx, int32_t n_programs, int32_t G, bool skip_const,
+                             int32_t p_lo, int32_t p_hi);
+
 // Shared front half of gp_evaluate / gp_predict: argument checks, staging, compile (stage),
 // Pearson shift, bucketing by stack need and the per-variant code streams (pack).
 static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_t*& offsets,
                          int32_t n_programs, int64_t n_nodes, int32_t max_stack, const float*& X,
                          int64_t ldx, int64_t n_rows, int32_t n_cols, int32_t G, bool pearson,
-                         const float* y, bool* any_host, bool skip_const = false) {
+                         const float* y, bool* any_host, bool skip_const = false,
+                         int32_t p_lo = 0, int32_t p_hi = -1) {
   if (n_programs < 1 || n_nodes < 1 || max_stack < 1 || max_stack > GP_MAX_STACK || n_rows < 1 ||
       n_cols < 1 || ldx < n_rows || !programs || !offsets || !X)
     return ctx->fail(GP_ERR_ARG, "invalid argument (n_programs=%d n_nodes=%lld max_stack=%d "
@@ -385,6 +399,14 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
                                     xref, stride, sh, ctx->stream), "shift kernel"))) return s;
     shift = sh;
   }
+  return bucket_pack(ctx, n_programs, G, skip_const, p_lo, p_hi < 0 ? n_programs : p_hi);
+}
+
+// Bucketing by stack need of the programs [p_lo, p_hi) (compiled by prepare) and the per-variant
+// code streams (pack).
+static gp_status bucket_pack(gp_context* ctx, int32_t n_programs, int32_t G, bool skip_const,
+                             int32_t p_lo, int32_t p_hi) {
+  gp_status s;
   int32_t* counts = (int32_t*)ctx->counts.p;
   int64_t* base = (int64_t*)(counts + 2 * kNumVariants);
   int subs[kNumVariants];  // row passes per program of each variant (its compiled shape)
@@ -392,7 +414,7 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   if ((s = ctx->launch(launch_bucket((const int32_t*)ctx->need.p, (const int32_t*)ctx->code_len.p,
                                    n_programs, G, subs, (int32_t*)ctx->lists.p, (int64_t*)ctx->pos.p,
                                    (int64_t*)ctx->gstart.p, counts, base, skip_const ? 1 : 0,
-                                   ctx->stream),
+                                   p_lo, p_hi, ctx->stream),
                      "bucket kernel"))) return s;
   return ctx->launch(launch_pack((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
                                (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->lists.p,
@@ -402,15 +424,122 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
                    "pack kernel");
 }
 
+// Population sharding (GP_SHARD_PROGRAMS): in-place all-gather of each rank's [lo, hi) fitness
+// and status through a padded buffer (world x chunk entries; ncclAllGather needs equal counts),
+// then back into place, so every rank holds all n results.
+static gp_status gather_programs(gp_context* ctx, int32_t n_programs, int32_t chunk, int32_t p_lo,
+                                 int32_t p_hi, float* fit_dev) {
+  gp_status s;
+  const size_t cb = (size_t)chunk * 4, own = (size_t)(p_hi - p_lo) * 4;
+  if ((s = ctx->grow(&ctx->gather.p, &ctx->gather.cap, 2 * (size_t)ctx->world * cb, "gather"))) return s;
+  char* gf = (char*)ctx->gather.p;
+  char* gs = gf + (size_t)ctx->world * cb;
+  if (own) {
+    if ((s = ctx->cuda(cudaMemcpyAsync(gf + ctx->rank * cb, fit_dev + p_lo, own, cudaMemcpyDeviceToDevice, ctx->stream), "gather in"))) return s;
+    if ((s = ctx->cuda(cudaMemcpyAsync(gs + ctx->rank * cb, (uint32_t*)ctx->status.p + p_lo, own, cudaMemcpyDeviceToDevice, ctx->stream), "gather in"))) return s;
+  }
+  NcclApi& n = nccl();
+  ncclResult_t r = n.AllGather(gf + ctx->rank * cb, gf, (size_t)chunk, ncclFloat32,
+                               (ncclComm_t)ctx->comm, ctx->stream);
+  if (r == ncclSuccess)
+    r = n.AllGather(gs + ctx->rank * cb, gs, (size_t)chunk, ncclUint32, (ncclComm_t)ctx->comm,
+                    ctx->stream);
+  if (r != ncclSuccess) return ctx->fail(GP_ERR_NCCL, "ncclAllGather: %s", n.GetErrorString(r));
+  if ((s = ctx->cuda(cudaMemcpyAsync(fit_dev, gf, (size_t)n_programs * 4, cudaMemcpyDeviceToDevice, ctx->stream), "gather out"))) return s;
+  return ctx->cuda(cudaMemcpyAsync(ctx->status.p, gs, (size_t)n_programs * 4, cudaMemcpyDeviceToDevice, ctx->stream), "gather out");
+}
+
+// Spearman fitness: per batch of programs the predict
+// kernels write yhat [B][m], spearman.cu ranks each row of it (ties averaged) and correlates the
+// ranks with rank(y) (weighted Pearson). Ranks need every row: with row sharding across ranks this
+// metric is refused; with GP_SHARD_PROGRAMS each rank ranks its own programs over all rows.
+static gp_status evaluate_spearman(gp_context* ctx, const gp_node* programs,
+                                   const int64_t* node_offsets, int32_t n_programs, int64_t n_nodes,
+                                   int32_t max_stack, const float* X, int64_t ldx, const float* y,
+                                   const float* w, int64_t n_rows, int32_t n_cols,
+                                   float* fitness_out, uint32_t* status_out, bool fit_host,
+                                   bool st_host, bool any_host) {
+  gp_status s;
+  const bool by_prog = ctx->comm && ctx->shard == GP_SHARD_PROGRAMS;
+  if (ctx->comm && !by_prog)
+    return ctx->fail(GP_ERR_UNSUPPORTED, "Spearman ranks need every row: use GP_SHARD_PROGRAMS");
+  if (n_rows > INT32_MAX / 2)
+    return ctx->fail(GP_ERR_ARG, "Spearman: n_rows %lld exceeds the int32 rank range", (long long)n_rows);
+  const int32_t m = (int32_t)n_rows;
+  const int32_t chunk = by_prog ? (n_programs + ctx->world - 1) / ctx->world : n_programs;
+  const int32_t p_lo = by_prog ? std::min(n_programs, ctx->rank * chunk) : 0;
+  const int32_t p_hi = by_prog ? std::min(n_programs, p_lo + chunk) : n_programs;
+  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, 1, true, false);
+  // compile every program (no bucket work yet: empty range)
+  if ((s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, n_rows,
+                   n_cols, pl.G, false, nullptr, &any_host, false, 0, 0))) return s;
+  // batch size: ~2 GB of per-row buffers (yhat, ranks, sort / scan scratch ~ 32 B per entry)
+  const int64_t budget = (int64_t)2 << 30;
+  int32_t B = (int32_t)std::max<int64_t>(1, std::min<int64_t>(std::max(1, p_hi - p_lo),
+                                                                budget / ((int64_t)m * 32)));
+  B = (int32_t)std::min<int64_t>(B, INT32_MAX / m);
+  if (const char* e = getenv("GP_SPEARMAN_BATCH")) B = std::max(1, std::min(B, atoi(e)));  // tests
+  const size_t scratch = std::max(rank_scratch_bytes(B, m), rank_scratch_bytes(1, m));
+  const int32_t Q = spearman_chunks(m);
+  const size_t bytes = (size_t)B * m * 4 * 2 + (size_t)m * 4 + (size_t)B * 4 +
+                       (size_t)B * Q * 6 * 8 + scratch + 1024;
+  if ((s = ctx->grow(&ctx->spear.p, &ctx->spear.cap, bytes, "spearman"))) return s;
+  char* p = (char*)ctx->spear.p;
+  double* part = (double*)p;                       p += (size_t)B * Q * 6 * 8;
+  float* yhat = (float*)p;                         p += (size_t)B * m * 4;
+  int32_t* rank2 = (int32_t*)p;                    p += (size_t)B * m * 4;
+  int32_t* ry2 = (int32_t*)p;                      p += (size_t)m * 4;
+  uint32_t* nonfin = (uint32_t*)p;                 p += (size_t)B * 4;
+  void* scr = (void*)(((uintptr_t)p + 255) & ~(uintptr_t)255);
+  // rank(y), once
+  if ((s = ctx->launch(launch_rank(y, 1, m, scr, scratch, ry2, nullptr, ctx->stream), "rank y"))) return s;
+  float* fit_dev = fitness_out;
+  if (fit_host) {
+    if ((s = ctx->grow(&ctx->h_fit.p, &ctx->h_fit.cap, (size_t)n_programs * sizeof(float), "fit"))) return s;
+    fit_dev = (float*)ctx->h_fit.p;
+  }
+  for (int32_t lo = p_lo; lo < p_hi; lo += B) {
+    const int32_t hi = std::min(p_hi, lo + B), nb = hi - lo;
+    if ((s = bucket_pack(ctx, n_programs, pl.G, false, lo, hi))) return s;
+    EvalArgs a{};
+    a.X = X;
+    a.ldx = ldx;
+    a.n_rows = n_rows;
+    a.n_cols = n_cols;
+    a.n_programs = n_programs;
+    a.metric = GP_MSE;
+    a.G = pl.G;
+    a.rows_per_chunk = pl.rows_per_chunk;
+    a.n_chunks = pl.n_chunks;
+    a.out = yhat - (int64_t)lo * m;                // predict writes out[p * m + i], p in [lo, hi)
+    a.ld_out = m;
+    if ((s = launch_variants(ctx, a, pl, max_stack, true))) return s;
+    if ((s = ctx->launch(launch_rank(yhat, nb, m, scr, scratch, rank2, nonfin, ctx->stream), "rank yhat"))) return s;
+    if ((s = ctx->launch(launch_spearman(rank2, ry2, w, nb, m, part, nonfin,
+                                       (const int32_t*)ctx->code_len.p + lo, fit_dev + lo,
+                                       (uint32_t*)ctx->status.p + lo, ctx->stream), "spearman"))) return s;
+  }
+  if (by_prog && (s = gather_programs(ctx, n_programs, chunk, p_lo, p_hi, fit_dev))) return s;
+  if (fit_host) {
+    if ((s = ctx->cuda(cudaMemcpyAsync(fitness_out, fit_dev, (size_t)n_programs * sizeof(float),
+                                       cudaMemcpyDeviceToHost, ctx->stream), "D2H fitness"))) return s;
+  }
+  if (status_out) {
+    if ((s = ctx->cuda(cudaMemcpyAsync(status_out, ctx->status.p, (size_t)n_programs * sizeof(uint32_t),
+                                       st_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                       ctx->stream), "status copy"))) return s;
+  }
+  if (any_host || fit_host || st_host) return ctx->cuda(cudaStreamSynchronize(ctx->stream), "sync");
+  return GP_OK;
+}
+
 gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
                       int32_t n_programs, int64_t n_nodes, int32_t max_stack, const float* X,
                       int64_t ldx, const float* y, const float* w, int64_t n_rows, int32_t n_cols,
                       gp_metric metric, float* fitness_out, uint32_t* status_out) {
   if (!ctx) return GP_ERR_ARG;
   cudaSetDevice(ctx->device);
-  if (metric == GP_SPEARMAN)
-    return ctx->fail(GP_ERR_UNSUPPORTED, "Spearman fitness is not on this hot path (SURVEY F1)");
-  if ((int)metric < 0 || (int)metric > GP_PEARSON || !y || !fitness_out)
+  if ((int)metric < 0 || (int)metric > GP_SPEARMAN || !y || !fitness_out)
     return ctx->fail(GP_ERR_ARG, "invalid metric / y / fitness_out");
   bool any_host = false;
   gp_status s;
@@ -423,13 +552,22 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
   }
   const bool fit_host = is_host_pointer(fitness_out);
   const bool st_host = status_out && is_host_pointer(status_out);
+  if (metric == GP_SPEARMAN)
+    return evaluate_spearman(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, y,
+                             w, n_rows, n_cols, fitness_out, status_out, fit_host, st_host,
+                             any_host);
   const int S = metric == GP_PEARSON ? 3 : 1;
   const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, S, false, w != nullptr);
-  // variable-free programs: closed form in finalize for MSE / RMSE / Pearson (not MAE, LogLoss)
-  const bool closed = ctx->const_programs &&
-                      (metric == GP_MSE || metric == GP_RMSE || metric == GP_PEARSON);
+  // variable-free programs: closed form in finalize for MSE / RMSE / LogLoss / Pearson (not MAE)
+  const bool closed = ctx->const_programs && metric != GP_MAE;
+  // population sharding: every rank holds all rows and evaluates the programs
+  // [lo, hi) of equal-count chunks; fitness / status are all-gathered after finalize
+  const bool by_prog = ctx->comm && ctx->shard == GP_SHARD_PROGRAMS;
+  const int32_t chunk = by_prog ? (n_programs + ctx->world - 1) / ctx->world : n_programs;
+  const int32_t p_lo = by_prog ? std::min(n_programs, ctx->rank * chunk) : 0;
+  const int32_t p_hi = by_prog ? std::min(n_programs, p_lo + chunk) : n_programs;
   if ((s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, n_rows,
-                   n_cols, pl.G, metric == GP_PEARSON, y, &any_host, closed))) return s;
+                   n_cols, pl.G, metric == GP_PEARSON, y, &any_host, closed, p_lo, p_hi))) return s;
 
   // Fused evaluation -> partial sums
   const int64_t ld_part = (int64_t)n_programs * S + 3;
@@ -453,13 +591,14 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
   a.y_shift = metric == GP_PEARSON ? (const float*)ctx->shift.p + n_programs : nullptr;
   ctx->last_plan = pl;
   if ((s = ctx->launch(launch_consts(y, w, n_rows, pl.rows_per_chunk, pl.n_chunks, a.y_shift,
-                                   a.partial, ld_part, (int64_t)n_programs * S, ctx->stream),
+                                   a.partial, ld_part, (int64_t)n_programs * S,
+                                   metric == GP_LOGLOSS ? 1 : 0, ctx->stream),
                      "consts kernel"))) return s;
   if ((s = launch_variants(ctx, a, pl, max_stack, false))) return s;
   if ((s = ctx->launch(launch_tile_reduce((const double*)ctx->partial.p, pl.n_chunks, ld_part,
                                         (double*)ctx->sums.p, ctx->stream), "tile_reduce"))) return s;
   // A6: one all-reduce of the fp64 partial sums across ranks (rows are sharded)
-  if (ctx->comm) {
+  if (ctx->comm && !by_prog) {
     NcclApi& n = nccl();
     ncclResult_t r = n.AllReduce(ctx->sums.p, ctx->sums.p, (size_t)ld_part, ncclFloat64, ncclSum,
                                  (ncclComm_t)ctx->comm, ctx->stream);
@@ -476,6 +615,7 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
                                      (const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
                                      closed ? 1 : 0, fit_dev,
                                      (uint32_t*)ctx->status.p, ctx->stream), "finalize"))) return s;
+  if (by_prog && (s = gather_programs(ctx, n_programs, chunk, p_lo, p_hi, fit_dev))) return s;
   if (fit_host) {
     if ((s = ctx->cuda(cudaMemcpyAsync(fitness_out, fit_dev, (size_t)n_programs * sizeof(float),
                                        cudaMemcpyDeviceToHost, ctx->stream), "D2H fitness"))) return s;

@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
                                                       int64_t* __restrict__ gstart,
                                                       int32_t* __restrict__ counts,
                                                       int64_t* __restrict__ base, int4 sub4,
-                                                      int32_t skip_const) {
+                                                      int32_t skip_const, int32_t p_lo,
+                                                      int32_t p_hi) {
   __shared__ int warp_cnt[kNumVariants][32];
   __shared__ int cnt[kNumVariants];
   __shared__ int64_t warp_tot[32];
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
   for (int c0 = 0; c0 < n; c0 += 1024) {
     const int p = c0 + tid;
     int b = -1;
-    if (p < n && code_len[p] > 0 && !(skip_const && need[p] == 0)) {
+    if (p >= p_lo && p < p_hi && code_len[p] > 0 && !(skip_const && need[p] == 0)) {
       b = kNumVariants - 1;
       for (int v = kNumVariants - 1; v >= 0; --v)
         if (need[p] <= caps[v]) b = v;
@@ -306,9 +307,10 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
 cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
                           int32_t G, const int* subs, int32_t* lists, int64_t* pos,
                           int64_t* gstart, int32_t* counts, int64_t* base, int32_t skip_const,
-                          cudaStream_t s) {
+                          int32_t p_lo, int32_t p_hi, cudaStream_t s) {
   bucket_kernel<<<1, 1024, 0, s>>>(need, code_len, n_programs, G, lists, pos, gstart, counts,
-                                   base, make_int4(subs[0], subs[1], subs[2], subs[3]), skip_const);
+                                   base, make_int4(subs[0], subs[1], subs[2], subs[3]), skip_const,
+                                   p_lo, p_hi);
   return cudaGetLastError();
 }
 
@@ -359,11 +361,13 @@ cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_
 
 // ---------------------------------------------------------------------------------------------
 // Dataset constants per row chunk (program independent): W = sum w, S_y = sum w (y - K_y),
-// S_yy = sum w (y - K_y)^2 over live rows (w != 0), fp64, fixed order.
+// S_yy = sum w (y - K_y)^2 over live rows (w != 0), fp64, fixed order. For LogLoss S_y is instead
+// W_1 = sum of w over rows with y > 1/2 (the rows the per-row loss scores as positives).
 // ---------------------------------------------------------------------------------------------
 __global__ void consts_kernel(const float* __restrict__ y, const float* __restrict__ w,
                               int64_t n_rows, int64_t rows_per_chunk, const float* y_shift,
-                              double* __restrict__ partial, int64_t ld_part, int64_t col0) {
+                              double* __restrict__ partial, int64_t ld_part, int64_t col0,
+                              int32_t logloss) {
   __shared__ double red[3][256];
   const int q = blockIdx.x, tid = threadIdx.x;
   const int64_t r0 = (int64_t)q * rows_per_chunk, r1 = min(r0 + rows_per_chunk, n_rows);
@@ -374,7 +378,7 @@ __global__ void consts_kernel(const float* __restrict__ y, const float* __restri
     if (wi != 0.0) {
       const double yc = (double)(y[i] - Ky);
       c0 += wi;
-      c1 += wi * yc;
+      c1 += logloss ? (y[i] > 0.5f ? wi : 0.0) : wi * yc;
       c2 += wi * yc * yc;
     }
   }
@@ -389,9 +393,9 @@ __global__ void consts_kernel(const float* __restrict__ y, const float* __restri
 
 cudaError_t launch_consts(const float* y, const float* w, int64_t n_rows, int64_t rows_per_chunk,
                           int64_t n_chunks, const float* y_shift, double* partial, int64_t ld_part,
-                          int64_t col0, cudaStream_t s) {
+                          int64_t col0, int32_t logloss, cudaStream_t s) {
   consts_kernel<<<(unsigned)n_chunks, 256, 0, s>>>(y, w, n_rows, rows_per_chunk, y_shift, partial,
-                                                    ld_part, col0);
+                                                    ld_part, col0, logloss);
   return cudaGetLastError();
 }
 
@@ -500,7 +504,18 @@ __global__ void finalize_kernel(const double* __restrict__ sums, int32_t n_progr
     out = metric == GP_PEARSON ? -INFINITY : INFINITY;
   } else if (metric != GP_PEARSON) {
     double f;
-    if (cst) {
+    if (cst && metric == GP_LOGLOSS) {
+      // the per-row loss of a constant prediction c is one of two values: softplus(-c) on rows
+      // with y > 1/2 (total weight W_1 = Sy here), softplus(c) on the others, each clamped to
+      // the p-clamp's range (C7)
+      const double c = (double)__uint_as_float(code[code_off[p]].y);
+      auto sp = [](double z) {
+        const double l = fmax(z, 0.0) + log1p(exp(-fabs(z)));
+        return l < 1.0000000000000005e-15 ? 1.0000000000000005e-15
+                                          : (l > 34.538776394910684 ? 34.538776394910684 : l);
+      };
+      f = isnan(c) ? c : (Sy * sp(-c) + (W - Sy) * sp(c)) / W;
+    } else if (cst) {
       const double c = (double)__uint_as_float(code[code_off[p]].y);
       f = (W * c * c - 2.0 * c * Sy + Syy) / W;
       if (f < 0.0) f = 0.0;                        // rounding; NaN / inf pass through

@@ -19,7 +19,7 @@ cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n
 cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
                           int32_t G, const int* subs, int32_t* lists, int64_t* pos,
                           int64_t* gstart, int32_t* counts, int64_t* base, int32_t skip_const,
-                          cudaStream_t s);
+                          int32_t p_lo, int32_t p_hi, cudaStream_t s);
 // Copies every bucketed program's code into its variant stream, flagging the end of each pass
 // and of each shared-memory stream window (kernels.h kEndWin).
 cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
@@ -29,7 +29,7 @@ cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_
 // Dataset constants W, S_y, S_yy per row chunk -> partial[q][col0 .. col0 + 2].
 cudaError_t launch_consts(const float* y, const float* w, int64_t n_rows, int64_t rows_per_chunk,
                           int64_t n_chunks, const float* y_shift, double* partial, int64_t ld_part,
-                          int64_t col0, cudaStream_t s);
+                          int64_t col0, int32_t logloss, cudaStream_t s);
 cudaError_t launch_shift(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                          int32_t n_programs, int32_t stack_cap, const float* xref,
                          int64_t xref_stride, float* shift_out, cudaStream_t s);
@@ -45,5 +45,20 @@ cudaError_t launch_select(const float* fitness, const int64_t* offsets, int32_t 
                           int32_t n_tournaments, int32_t k, float parsimony, int32_t higher,
                           uint64_t seed, uint32_t generation, int32_t* winners, cudaStream_t s);
 cudaError_t launch_copy_scalar(const float* src, float* dst, cudaStream_t s);
+
+// ---- Spearman (spearman.cu) ----------------------------------------------------------
+// Doubled tie-averaged ranks of B segments of m fp32 keys (B m <= INT32_MAX):
+// rank2[b m + i] = 2 rank of keys[b m + i] within segment b; nonfinite[b] (optional) = any
+// non-finite key in segment b. scratch >= rank_scratch_bytes(B, m) device bytes.
+size_t rank_scratch_bytes(int32_t B, int32_t m);
+cudaError_t launch_rank(const float* keys, int32_t B, int32_t m, void* scratch,
+                        size_t scratch_bytes, int32_t* rank2, uint32_t* nonfinite, cudaStream_t s);
+// Weighted Pearson of rank2 [B][m] against ry2 [m] -> fitness[b], status[b] (|= undefined
+// flag); part: [B][spearman_chunks(m)][6] fp64 scratch. code_len[b] == 0 -> -inf.
+int32_t spearman_chunks(int32_t m);
+cudaError_t launch_spearman(const int32_t* rank2, const int32_t* ry2, const float* w, int32_t B,
+                            int32_t m, double* part, const uint32_t* nonfinite,
+                            const int32_t* code_len, float* fitness, uint32_t* status,
+                            cudaStream_t s);
 
 }  // namespace gpb

@@ -13,7 +13,12 @@
 //   purpose 1: mutation kind of child i;  purpose 2: mutation internals of child i;
 //   purpose 3: initial program i;  purpose 0: tournaments (device kernel).
 #include <algorithm>
+#include <array>
 #include <chrono>
+#include <mutex>
+#include <memory>
+#include <functional>
+#include <condition_variable>
 #include <cmath>
 #include <cstring>
 #include <thread>
@@ -195,21 +200,78 @@ Prog subtree_mutation(Rng& st, const Prog& parent, const gp_config& c, int n_fea
   return hoisted_crossover(st, parent, donor, c);
 }
 
+// Persistent worker pool for the host steps of a generation (kinds, mutations, flattening): the
+// workers are created once per engine, so a generation pays a wake-up, not thread creation.
+// Work split is static (contiguous index ranges), so results never depend on scheduling.
+class Pool {
+ public:
+  explicit Pool(int n) {
+    for (int t = 1; t < n; ++t) workers_.emplace_back([this, t] { loop(t); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++epoch_;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  int size() const { return (int)workers_.size() + 1; }
+  // runs body(t) for t in [0, parts) on the caller + workers, returns when all are done
+  void run(int parts, const std::function<void(int)>& body) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      body_ = &body;
+      parts_ = parts;
+      pending_ = (int)workers_.size();
+      ++epoch_;
+    }
+    cv_.notify_all();
+    if (parts > 0) body(0);
+    std::unique_lock<std::mutex> l(m_);
+    done_.wait(l, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void loop(int t) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* body;
+      int parts;
+      {
+        std::unique_lock<std::mutex> l(m_);
+        cv_.wait(l, [&] { return epoch_ != seen; });
+        seen = epoch_;
+        if (stop_) return;
+        body = body_;
+        parts = parts_;
+      }
+      if (t < parts) (*body)(t);
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* body_ = nullptr;
+  int parts_ = 0, pending_ = 0;
+  uint64_t epoch_ = 0;
+  bool stop_ = false;
+};
+
 template <class F>
-void parallel_for(int n, int threads, F&& f) {
+void parallel_for(Pool* pool, int n, F&& f) {
+  const int threads = pool ? std::min(pool->size(), (n + 31) / 32) : 1;
   if (threads <= 1 || n < 64) {
     for (int i = 0; i < n; ++i) f(i);
     return;
   }
-  threads = std::min(threads, (n + 31) / 32);
-  std::vector<std::thread> pool;
-  pool.reserve(threads);
-  for (int t = 0; t < threads; ++t)
-    pool.emplace_back([&, t] {
-      const int b = (int)((int64_t)n * t / threads), e = (int)((int64_t)n * (t + 1) / threads);
-      for (int i = b; i < e; ++i) f(i);
-    });
-  for (auto& th : pool) th.join();
+  pool->run(threads, [&](int t) {
+    const int b = (int)((int64_t)n * t / threads), e = (int)((int64_t)n * (t + 1) / threads);
+    for (int i = b; i < e; ++i) f(i);
+  });
 }
 
 double now_s() {
@@ -223,6 +285,7 @@ struct gp_engine {
   gp_config cfg{};
   bool higher = false;
   int threads = 1;
+  std::unique_ptr<Pool> pool;    // host worker pool (threads - 1 workers + the caller)
   // dataset (device views; owned copies when the caller passed host memory)
   const float *X = nullptr, *y = nullptr, *w = nullptr;
   int64_t ldx = 0, n_rows = 0;
@@ -319,37 +382,43 @@ struct gp_engine {
     }
     h_off[0] = 0;
     for (int i = 0; i < n; ++i) h_off[i + 1] = h_off[i] + (int64_t)pop[i].size();
-    parallel_for(n, threads, [&](int i) {
-      std::memcpy(h_nodes + h_off[i], pop[i].data(), pop[i].size() * sizeof(gp_node));
+    // per program (parallel): flatten into the pinned CSR, stack need, and the opcode histogram of
+    // variable-dependent nodes (per-row work; variable-free subtrees are per-program constants)
+    std::vector<std::array<int32_t, GP_OP_COUNT + 2>> hist(n);  // [ops..., const nodes, const prog]
+    parallel_for(pool.get(), n, [&](int i) {
+      const Prog& pr = pop[i];
+      std::memcpy(h_nodes + h_off[i], pr.data(), pr.size() * sizeof(gp_node));
       int d;
-      shape(pop[i], &d, &needs[i]);
-    });
-    max_need = 1;
-    for (int v : needs) max_need = std::max(max_need, v);
-    // opcode histogram of variable-dependent nodes (per-row work); variable-free subtrees are
-    // per-program constants and are counted separately
-    std::fill(op_count, op_count + GP_OP_COUNT, (int64_t)0);
-    const_nodes = 0;
-    const_programs = 0;
-    std::vector<char> is_const;
-    for (int p = 0; p < n; ++p) {
-      const Prog& pr = pop[p];
-      is_const.assign(pr.size(), 0);
+      shape(pr, &d, &needs[i]);
+      auto& h = hist[i];
+      h.fill(0);
+      std::vector<char> is_const(pr.size(), 0);
       std::vector<int64_t> kids;  // reverse-prefix stack of child indices
-      for (int64_t i = (int64_t)pr.size() - 1; i >= 0; --i) {
-        const int op = pr[i].op;
+      kids.reserve(pr.size());
+      for (int64_t k = (int64_t)pr.size() - 1; k >= 0; --k) {
+        const int op = pr[k].op;
         const int ar = arity(op);
         bool c = op == GP_OP_CONST;
         if (ar > 0) {
           c = true;
-          for (int k = 0; k < ar; ++k) { c = c && is_const[kids.back()]; kids.pop_back(); }
+          for (int j = 0; j < ar; ++j) { c = c && is_const[kids.back()]; kids.pop_back(); }
         }
-        is_const[i] = c;
-        kids.push_back(i);
-        if (c) ++const_nodes;
-        else if (op >= 0 && op < GP_OP_COUNT) ++op_count[op];
+        is_const[k] = c;
+        kids.push_back(k);
+        if (c) ++h[GP_OP_COUNT];
+        else if (op >= 0 && op < GP_OP_COUNT) ++h[op];
       }
-      if (!pr.empty() && is_const[0]) ++const_programs;
+      h[GP_OP_COUNT + 1] = !pr.empty() && is_const[0];
+    });
+    max_need = 1;
+    for (int v : needs) max_need = std::max(max_need, v);
+    std::fill(op_count, op_count + GP_OP_COUNT, (int64_t)0);
+    const_nodes = 0;
+    const_programs = 0;
+    for (int i = 0; i < n; ++i) {
+      for (int k = 0; k < GP_OP_COUNT; ++k) op_count[k] += hist[i][k];
+      const_nodes += hist[i][GP_OP_COUNT];
+      const_programs += hist[i][GP_OP_COUNT + 1];
     }
     n_nodes = total;
     gp_status s;
@@ -441,7 +510,7 @@ gp_status gp_engine_create(gp_engine** out, gp_context* ctx, const gp_config* cf
   const gp_config& c = *cfg;
   const double psum = c.p_crossover + c.p_subtree + c.p_hoist + c.p_point;
   bool ok = c.population_size >= 1 && c.tournament_size >= 1 && c.metric >= 0 &&
-            c.metric <= GP_PEARSON && c.n_functions >= 1 && c.n_functions <= 32 &&
+            c.metric <= GP_SPEARMAN && c.n_functions >= 1 && c.n_functions <= 32 &&
             c.init_depth_min >= 1 && c.init_depth_max >= c.init_depth_min &&
             c.stack_capacity >= 2 && c.stack_capacity <= GP_MAX_STACK &&
             c.init_depth_max <= c.stack_capacity - 1 && psum <= 1.0 + 1e-9 && c.p_crossover >= 0 &&
@@ -452,8 +521,10 @@ gp_status gp_engine_create(gp_engine** out, gp_context* ctx, const gp_config* cf
   gp_engine* e = new gp_engine();
   e->ctx = ctx;
   e->cfg = c;
-  e->higher = c.metric == GP_PEARSON;
+  e->higher = c.metric == GP_PEARSON || c.metric == GP_SPEARMAN;  // correlations: higher wins
   e->threads = c.n_threads > 0 ? c.n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  // one generation's host work is O(population); beyond 64 threads wake-ups cost more than they save
+  e->pool.reset(new Pool(std::min(e->threads, 64)));
   gp_status s = e->set_dataset(X, ldx, y, w, n_rows, n_cols);
   if (s) { delete e; return s; }
   *out = e;
@@ -483,7 +554,7 @@ gp_status gp_engine_init_population(gp_engine* e, gp_generation_stats* stats_out
   const gp_config& c = e->cfg;
   const int n = c.population_size;
   e->pop.assign(n, Prog());
-  parallel_for(n, e->threads, [&](int i) {
+  parallel_for(e->pool.get(), n, [&](int i) {
     Rng r(c.seed, (uint32_t)i, 0u, 3u);
     const int method = i < n / 2 ? FULL : GROW;
     const int md = c.init_depth_min + i % (c.init_depth_max - c.init_depth_min + 1);
@@ -513,7 +584,7 @@ gp_status gp_generation(gp_engine* e, gp_generation_stats* stats_out) {
   const uint32_t g = (uint32_t)(e->generation + 1);
   // (1) mutation kinds first, so the tournament count is known
   e->kinds.resize(n);
-  parallel_for(n, e->threads, [&](int i) {
+  parallel_for(e->pool.get(), n, [&](int i) {
     Rng r(c.seed, (uint32_t)i, g, 1u);
     const double u = r.uniform();
     const double p[4] = {c.p_crossover, c.p_subtree, c.p_hoist, c.p_point};
@@ -542,7 +613,7 @@ gp_status gp_generation(gp_engine* e, gp_generation_stats* stats_out) {
   // (3) host mutations, one Philox stream per child
   std::vector<Prog> next(n);
   const int nf = e->n_cols;
-  parallel_for(n, e->threads, [&](int i) {
+  parallel_for(e->pool.get(), n, [&](int i) {
     Rng r(c.seed, (uint32_t)i, g, 2u);
     const Prog& parent = e->pop[e->winners[toff[i]]];
     switch (e->kinds[i]) {

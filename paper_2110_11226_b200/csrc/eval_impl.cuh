@@ -37,6 +37,9 @@
 #ifndef GP_MINB
 #define GP_MINB 1   // minimum resident CTAs per SM (register budget = 64K / (GP_MINB * NT))
 #endif
+#ifndef GP_RED_ROWS
+#define GP_RED_ROWS 16  // programs per warp reduction block (32 / GP_RED_ROWS lanes per program)
+#endif
 
 #define GP_CAT2(a, b) a##b
 #define GP_CAT(a, b) GP_CAT2(a, b)
@@ -47,6 +50,8 @@ namespace GP_NS {
 
 constexpr int STACK = GP_STACK, R = GP_R, SUB = GP_SUB, NT = GP_NT;
 constexpr int TILE = NT * R * SUB, NW = NT / 32, R4 = R / 4;
+constexpr int RR = GP_RED_ROWS, LPR = 32 / RR, RED_BYTES = NW * RR * kRedStride * 4;
+static_assert(RR == 8 || RR == 16, "reduction block: 8 or 16 programs");
 static_assert(R % 4 == 0 && NT % 32 == 0, "R must be a multiple of 4");
 static_assert(TILE == kTile, "every variant shares the row tile");
 static_assert(STACK <= kCaseStride, "slot must fit the case stride");
@@ -61,9 +66,8 @@ constexpr float kLogLossHi = 34.538776394910684f;      // -ln(1e-15)
 // Shared-memory layout (bytes): fp64 accumulators [NW][G][S] | reduction blocks [NW][kRedRows]
 // [kRedStride] fp32 | ys[TILE] | ws[TILE] (weighted only) | xs[n_cols][TILE] (small n_cols only)
 // | code-stream window [kStreamWin + 2] uint4
-static_assert(kRedBytes == NW * kRedRows * kRedStride * 4, "reduction block size");
 __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
-  return (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15) + kRedBytes;
+  return (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15) + RED_BYTES;
 }
 
 #define LBL(OPV, s) ((OPV) * kCaseStride + (s))
@@ -208,9 +212,9 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
   const int n_groups = (count + a.G - 1) / a.G;
   const int64_t n_items = (int64_t)n_groups * a.n_chunks;
   double* acc = reinterpret_cast<double*>(smem);                 // [NW][G][S]
-  // this warp's transposed reduction block [kRedRows][kRedStride] (single-sum metrics)
-  float* rbw = reinterpret_cast<float*>(smem + (PREDICT ? 0 : smem_acc_bytes(a.G, S) - kRedBytes)) +
-               warp * (kRedRows * kRedStride);
+  // this warp's transposed reduction block [RR][kRedStride] (single-sum metrics)
+  float* rbw = reinterpret_cast<float*>(smem + (PREDICT ? 0 : smem_acc_bytes(a.G, S) - RED_BYTES)) +
+               warp * (RR * kRedStride);
   const bool has_w = a.w != nullptr;
   // global-X path: 16-byte vector loads when every column start is 16-byte aligned
   const bool x_vec = ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && ((a.ldx & 3) == 0);
@@ -264,19 +268,25 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
       const bool fast_mse = !PREDICT && (a.metric == GP_MSE || a.metric == GP_RMSE) && !has_w &&
                             nvalid == TILE;
       // Single-sum metrics (A5): each lane stores its fp32 sum of a finished program into row
-      // (slot % kRedRows) of the warp's block; every kRedRows programs the warp reduces the
-      // block at once -- lane L sums half a row (4 LDS.128), one shuffle joins the halves, and
-      // the even lanes add the kRedRows program sums into their fp64 accumulators. Fixed order
-      // -> deterministic. (Replaces one shuffle butterfly per program.)
+      // (slot % RR) of the warp's block; every RR programs the warp reduces the block at once --
+      // LPR lanes per row each sum 32 / LPR values (LDS.128, conflict-free with the padded
+      // stride), log2(LPR) shuffles join them, and the row's first lane adds the program sum into
+      // its fp64 accumulator. Fixed order -> deterministic. (Replaces one shuffle butterfly per
+      // program.)
       auto flush = [&](int p0, int n) {
         __syncwarp();
-        const int row = lane >> 1, half = lane & 1;
-        const float4* src = reinterpret_cast<const float4*>(rbw + row * kRedStride + half * 16);
-        const float4 v0 = src[0], v1 = src[1], v2 = src[2], v3 = src[3];
-        float m = ((v0.x + v0.y) + (v0.z + v0.w)) + ((v1.x + v1.y) + (v1.z + v1.w)) +
-                  (((v2.x + v2.y) + (v2.z + v2.w)) + ((v3.x + v3.y) + (v3.z + v3.w)));
-        m += __shfl_xor_sync(0xffffffffu, m, 1);
-        if (half == 0 && row < n) acc[(size_t)warp * a.G + p0 + row] += (double)m;
+        const int row = lane / LPR, part = lane % LPR;
+        const float4* src =
+            reinterpret_cast<const float4*>(rbw + row * kRedStride + part * (32 / LPR));
+        float m = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8 / LPR; k += 2) {
+          const float4 u = src[k], v = src[k + 1];
+          m += ((u.x + u.y) + (u.z + u.w)) + ((v.x + v.y) + (v.z + v.w));
+        }
+#pragma unroll
+        for (int o = 1; o < LPR; o <<= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+        if (part == 0 && row < n) acc[(size_t)warp * a.G + p0 + row] += (double)m;
         __syncwarp();
       };
       float st[STACK][R];
@@ -334,6 +344,9 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
       // end of one row pass of the program in group slot `pslot`: prediction store or loss
       int pslot = 0;
       auto end_pass = [&]() {
+        // one pass per program: the loss starts from zero here (folds into the first FFMA2)
+        // instead of being reset after the reduction
+        if constexpr (SUB == 1) { l0 = l1 = l2 = 0.f; }
         if constexpr (PREDICT) {
           float* o = a.out + (int64_t)gids[pslot] * a.ld_out + t0;
 #pragma unroll
@@ -381,23 +394,23 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
           if (cw.w) {                                // last word of a row pass or of the window
             if (cw.w & (kEndPass | kEndProgram)) {
               end_pass();
-              if (cw.w & kEndPass) {                 // next row pass of the same program
+              if (SUB > 1 && (cw.w & kEndPass)) {    // next row pass of the same program
                 ebase = (int)(cw.w >> 8) * NT * R + tid * 4;
               } else {                               // program done (A5)
                 if constexpr (!PREDICT) {
                   const int j = (int)(cw.w >> 8);    // == pslot
                   if (S == 1) {
-                    rbw[(j % kRedRows) * kRedStride + lane] = l0 + l1;  // l1: odd rows (MSE)
-                    if (j % kRedRows == kRedRows - 1) flush(j - (kRedRows - 1), kRedRows);
+                    rbw[(j % RR) * kRedStride + lane] = l0 + l1;  // l1: odd rows (MSE)
+                    if (j % RR == RR - 1) flush(j - (RR - 1), RR);
                   } else {
                     double* slot = acc + ((size_t)warp * a.G + j) * S;
                     const double v0 = warp_sum_f64(l0), v1 = warp_sum_f64(l1),
                                  v2 = warp_sum_f64(l2);
                     if (lane == 0) { slot[0] += v0; slot[1] += v1; slot[2] += v2; }
                   }
-                  l0 = l1 = l2 = 0.f;
+                  if constexpr (SUB > 1) { l0 = l1 = l2 = 0.f; }
                 }
-                ebase = tid * 4;
+                if constexpr (SUB > 1) ebase = tid * 4;
                 ++pslot;
               }
             }
@@ -405,8 +418,8 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB -
           }
         }
       }
-      if (!PREDICT && S == 1 && np % kRedRows != 0)  // last partial block of the tile
-        flush(np - np % kRedRows, np % kRedRows);
+      if (!PREDICT && S == 1 && np % RR != 0)        // last partial block of the tile
+        flush(np - np % RR, np % RR);
     }
 
     if constexpr (!PREDICT) {
@@ -457,7 +470,7 @@ static int occupancy(bool predict, bool xsmem, size_t smem) {
 
 const EvalVariant& GP_CAT(eval_variant_, GP_NS)() {
   static const EvalVariant v = {EvalShape{GP_NS::STACK, GP_NS::R, GP_NS::SUB, GP_NS::NT},
-                                &GP_NS::launch, &GP_NS::occupancy};
+                                &GP_NS::launch, &GP_NS::occupancy, &GP_NS::smem_acc_bytes};
   return v;
 }
 

@@ -35,7 +35,7 @@ struct gp_context {
   void* comm = nullptr;  // ncclComm_t
   std::string err;
   // device workspaces (grown on demand, stream-ordered)
-  gpb::StageBuf code, code_off, code_len, need, lists, pos, gstart, counts, codestream, scratch, status, partial,
+  gpb::StageBuf gather, spear, code, code_off, code_len, need, lists, pos, gstart, counts, codestream, scratch, status, partial,
       sums, shift, xref;
   // staging for [host] arguments
   gpb::StageBuf h_nodes, h_off, h_X, h_y, h_w, h_fit;
@@ -50,9 +50,10 @@ struct gp_context {
   int64_t kernel_launches = 0;   // gp_context_kernel_launches
   bool sethi_ullman = true;      // gp_context_set_eval_order
   bool const_programs = true;    // gp_context_set_const_programs (closed-form constant programs)
+  gp_shard shard = GP_SHARD_ROWS;  // gp_context_set_shard
 
   std::vector<gpb::StageBuf*> all_buffers() {
-    return {&code, &code_off, &code_len, &need, &lists, &pos, &gstart, &counts, &codestream, &scratch, &status,
+    return {&gather, &spear, &code, &code_off, &code_len, &need, &lists, &pos, &gstart, &counts, &codestream, &scratch, &status,
             &partial, &sums, &shift, &xref,
             &h_nodes, &h_off, &h_X, &h_y, &h_w, &h_fit};
   }

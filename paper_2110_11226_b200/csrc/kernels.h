@@ -25,11 +25,10 @@ constexpr int kVariantStack[kNumVariants] = {4, 8, 12, 20};
 constexpr uint32_t kEndPass = 1u, kEndProgram = 2u, kEndWin = 4u;
 // Code-stream window staged in shared memory per CTA (words of 16 B).
 constexpr int kStreamWin = 768;
-// Per-warp transposed reduction block of the single-sum metrics (eval_impl.cuh): kRedRows
-// programs x 32 lanes of fp32 per-lane sums, rows padded to kRedStride floats so the
-// row-half LDS.128 reads of a warp hit 32 distinct banks.
-constexpr int kRedRows = 16, kRedStride = 36;
-constexpr int kRedBytes = 4 * kRedRows * kRedStride * 4;  // 4 warps per CTA (NT = 128)
+// Per-warp transposed reduction block of the single-sum metrics (eval_impl.cuh): GP_RED_ROWS
+// programs x 32 lanes of fp32 per-lane sums, rows padded to kRedStride floats so the row-part
+// LDS.128 reads of a warp hit 32 distinct banks.
+constexpr int kRedStride = 36;
 
 // Everything the fused evaluator needs for one launch (see eval_impl.cuh). Each variant runs a
 // packed CODE STREAM per program group: for every program of the group, SUB copies of its code
@@ -79,6 +78,9 @@ struct EvalVariant {
                         cudaStream_t s);
   // Resident CTAs per SM for the given dynamic shared memory.
   int (*occupancy)(bool predict, bool xsmem, size_t smem);
+  // Shared memory of the fp64 accumulators + reduction blocks for G programs, S sums each
+  // (FIT mode; precedes the tiles in the kernel's layout).
+  size_t (*acc_bytes)(int G, int S);
 };
 const EvalVariant& eval_variant_s4();
 const EvalVariant& eval_variant_s8();

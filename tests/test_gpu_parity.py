@@ -298,8 +298,15 @@ def test_edge_cases(gp, ctx, orc):
     fw, _ = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), dev(w), metric="mse", max_stack=8)
     rw, _, _ = orc.population_fitness(nodes, off, X, y, w, "mse")
     assert abs(fw.cpu().numpy()[0] - rw[0]) <= 1e-4 * rw[0]
+    # Spearman ranks need every row: refused on a row-sharded communicator context
+    c1 = gp.Context(0, unique_id=gp.get_unique_id(), rank=0, world_size=1)
     with pytest.raises(gp.GPError):
-        ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="spearman", max_stack=8)
+        c1.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="spearman", max_stack=8)
+    c1.set_shard("programs")
+    f1, _ = c1.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="spearman", max_stack=8)
+    f0, _ = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="spearman", max_stack=8)
+    assert torch.equal(f0, f1)
+    c1.close()
 
 
 # ---- tournament selection: bit-exact against the oracle replay --------------------------------------
@@ -336,6 +343,12 @@ def test_single_rank_nccl_context_matches(gp, ctx):
     for metric in ("mse", "pearson"):
         a, sa = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric=metric, max_stack=8)
         b, sb = c1.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric=metric, max_stack=8)
+        assert torch.equal(a, b) and torch.equal(sa, sb)
+        # population sharding (F3) on one rank: the program chunk is everything and the
+        # fitness / status all-gather is an exact identity
+        c1.set_shard("programs")
+        b, sb = c1.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric=metric, max_stack=8)
+        c1.set_shard("rows")
         assert torch.equal(a, b) and torch.equal(sa, sb)
     assert c1.kernel_launches() > 0
     c1.close()
@@ -382,3 +395,75 @@ def test_constant_programs_match_oracle(gp, ctx, orc, metric, weighted):
     fin = np.isfinite(a) & np.isfinite(b)
     assert np.array_equal(np.isfinite(a), np.isfinite(b))
     assert np.all(np.abs(a[fin] - b[fin]) <= 1e-5 * np.maximum(np.abs(b[fin]), 1e-6))
+
+
+# ---- Spearman -------------------------------------------
+def _integer_case(n_rows, n_prog, seed):
+    """Integer-valued data and {add, sub, mul} programs with integer constants, depth <= 3: every
+    fp32 evaluation is exact, so the GPU ranks exactly what the oracle ranks (ties included)."""
+    rng = np.random.default_rng(seed)
+    X = rng.integers(-4, 5, (2, n_rows)).astype(np.float32)
+    y = (X[0] * X[1] + rng.integers(-3, 4, n_rows)).astype(np.float32)
+    nodes, off = synth.random_population(n_prog, seed=seed, depth=(0, 3), funcs=(2, 3, 4),
+                                         n_features=2, max_stack=8)
+    nodes = nodes.copy()
+    c = nodes[:, 0] == synth.CONST
+    nodes[c, 1] = rng.integers(-3, 4, int(c.sum())).astype(np.float32).view(np.int32)
+    return X, y, nodes, off
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+@pytest.mark.parametrize("batch", [None, 7])
+def test_spearman_exact_inputs_match_oracle(gp, ctx, orc, weighted, batch, monkeypatch):
+    n_rows = 2 * 2048 + 999
+    X, y, nodes, off = _integer_case(n_rows, 90, seed=12)
+    w = synth.weights(n_rows, seed=3) if weighted else None
+    if batch:
+        monkeypatch.setenv("GP_SPEARMAN_BATCH", str(batch))      # several program batches
+    fit, st = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), None if w is None else dev(w),
+                           metric="spearman", max_stack=8)
+    torch.cuda.synchronize()
+    ref, _, flags = orc.population_fitness(nodes, off, X, y, w, "spearman")
+    g, s = fit.cpu().numpy(), st.cpu().numpy()
+    for p in range(len(ref)):
+        if flags[p] & F_UND:
+            assert g[p] == 0.0 and s[p] & 16, p               # undefined -> 0 + GP_FLAG_UNDEFINED_CORR
+        else:
+            assert abs(float(g[p]) - ref[p]) <= 1e-6 + 2 ** -24 * abs(ref[p]), (p, g[p], ref[p])
+    assert np.count_nonzero(flags & F_UND) < len(ref)
+
+
+def test_spearman_general_programs(gp, ctx, orc):
+    """Random Table 2 programs on the Pagie grid: fp32 rounding may reorder rows whose values
+    differ by less than the evaluation error, which moves r by O(swaps / n); the bulk must agree
+    to 1e-4 and every program to 2e-3."""
+    X, y = synth.pagie_grid(64)
+    nodes, off = synth.random_population(150, seed=77, depth=(1, 6), max_stack=8)
+    fit, st = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric="spearman", max_stack=8)
+    ref, _, flags = orc.population_fitness(nodes, off, X, y, None, "spearman")
+    g = fit.cpu().numpy().astype(np.float64)
+    ok = (flags & (F_OVF | F_AMB | F_UND)) == 0
+    d = np.abs(g[ok] - ref[ok])
+    assert np.all(d <= 2e-3), d.max()
+    assert np.mean(d <= 1e-4 * np.maximum(np.abs(ref[ok]), 1e-2)) >= 0.9
+
+
+def test_spearman_engine_selects_highest(gp, ctx, orc):
+    """gp_generation with Spearman: higher is better in the tournaments (teacher-forced against the
+    oracle's replay on the GPU's own fitness)."""
+    from oracle import engine as oe
+    X, y = synth.pagie_grid(32)
+    e = gp.Engine(ctx, dev(X), dev(y), population_size=64, metric="spearman", seed=11)
+    ocfg = oe.Config(population_size=64, metric="spearman", seed=11)
+    e.init_population()
+    nodes, off, fit = e.population()
+    opop = oe.ramped_init(ocfg)
+    for g in range(1, 4):
+        e.generation()
+        kinds, winners = e.last_selection()
+        rec = oe.next_generation(opop, fit, ocfg, g, True)
+        assert np.array_equal(winners, rec.winners) and kinds.tolist() == rec.kinds
+        nodes, off, fit = e.population()
+        on, oo = oe.flatten(rec.population)
+        assert np.array_equal(nodes, on) and np.array_equal(off, oo)
+        opop = rec.population

@@ -95,3 +95,65 @@ def test_two_rank_sharded_fitness_gloo():
         errs.append(errq.get())
     assert not errs, "\n".join(errs)
     assert all(p.exitcode == 0 for p in procs)
+
+
+def _program_chunk(n, rank, world):
+    """The program range of one rank under GP_SHARD_PROGRAMS (include/gp.h, api.cpp
+    gp_evaluate): equal-count chunks c = ceil(n / world), rank r owns [min(n, r c), min(n, r c + c))."""
+    c = (n + world - 1) // world
+    lo = min(n, rank * c)
+    return c, lo, min(n, lo + c)
+
+
+def _worker_programs(rank, world, port, errq, n_programs):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import bench
+        import oracle
+        import synth
+        cfg = dict(bench.CONFIGS["c1"])
+        X, y, _, _, m = bench.load_dataset(cfg, 0, 1)            # every rank holds all rows
+        nodes, off = synth.random_population(n_programs, seed=9, depth=(1, 5))
+        c, lo, hi = _program_chunk(n_programs, rank, world)
+        # this rank's chunk in a padded world x c buffer, combined by an all-gather
+        mine = torch.full((c,), float("nan"), dtype=torch.float64)
+        for p in range(lo, hi):
+            v, _, _ = oracle.eval_program(nodes[off[p]:off[p + 1]], X)
+            mine[p - lo] = oracle.fitness("mse", v, y, None)[0]
+        parts = [torch.empty(c, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        fit = torch.cat(parts)[:n_programs].numpy()
+        for p in range(n_programs):
+            v, _, _ = oracle.eval_program(nodes[off[p]:off[p + 1]], X)
+            assert fit[p] == oracle.fitness("mse", v, y, None)[0], p
+        # every program owned by exactly one rank
+        owned = torch.zeros(n_programs, dtype=torch.int64)
+        owned[lo:hi] = 1
+        dist.all_reduce(owned)
+        assert bool((owned == 1).all())
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        errq.put(f"rank {rank}: {e}\n{traceback.format_exc()}")
+        raise
+
+
+@pytest.mark.parametrize("world,n_programs", [(2, 13), (3, 2)])
+def test_program_sharded_fitness_gloo(world, n_programs):
+    """SURVEY F3 host logic: program chunks (ragged last chunk; an empty chunk when world > n)
+    evaluated per rank and all-gathered give the whole population's fitness on every rank."""
+    ctx = mp.get_context("spawn")
+    errq = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_programs, args=(r, world, port, errq, n_programs))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, "\n".join(errs)
+    assert all(p.exitcode == 0 for p in procs)
