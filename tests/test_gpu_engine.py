@@ -95,6 +95,41 @@ def test_full_size_c3_sampled(gp, ctx, orc):
     check_fitness(fit[sample], ref, sens, flags, "mse", max_excluded=1.0)
 
 
+def test_full_size_c3_decomposition_invariant(gp, ctx):
+    """Every program of the C3 population at full size (bench launch configuration: groups of 128
+    programs whose code streams span several shared-memory windows, 16-program reduction blocks)
+    against the same programs evaluated 8 at a time (groups of 8, one window): the work
+    decomposition only changes the fp32 / fp64 summation order. Constant programs are compared
+    between the closed form and the per-row path as well."""
+    X, y = synth.pagie_grid(4096)
+    Xd, yd = dev(X), dev(y)
+    e = gp.Engine(ctx, Xd, yd, population_size=8192, metric="mse", seed=2110)
+    e.init_population()
+    e.generation()
+    nodes, off, fit = e.population()
+    e.close()
+    nd, of = dev(nodes), dev(off)
+    full, _ = ctx.evaluate(nd, of, Xd, yd, metric="mse", max_stack=20)
+    ctx.set_const_programs(False)
+    try:
+        rows, _ = ctx.evaluate(nd, of, Xd, yd, metric="mse", max_stack=20)
+    finally:
+        ctx.set_const_programs(True)
+    full, rows = full.cpu().numpy(), rows.cpu().numpy()
+    assert np.array_equal(full, fit)                  # the engine's own evaluation
+    fin = np.isfinite(full)
+    assert np.array_equal(fin, np.isfinite(rows))
+    assert np.all(np.abs(full[fin] - rows[fin]) <= 1e-5 * np.maximum(np.abs(full[fin]), 1e-6))
+    part = np.empty_like(full)
+    for p0 in range(0, len(off) - 1, 8):
+        sub = nodes[off[p0]:off[min(p0 + 8, len(off) - 1)]]
+        so = off[p0:min(p0 + 8, len(off) - 1) + 1] - off[p0]
+        f, _ = ctx.evaluate(dev(sub), dev(so), Xd, yd, metric="mse", max_stack=20)
+        part[p0:p0 + len(so) - 1] = f.cpu().numpy()
+    assert np.array_equal(np.isfinite(part), fin)
+    assert np.all(np.abs(full[fin] - part[fin]) <= 1e-5 * np.maximum(np.abs(full[fin]), 1e-6))
+
+
 @pytest.mark.parametrize("cfg", ["c4", "c5"])
 def test_full_size_wide_configs_sampled(gp, ctx, orc, cfg):
     """C4 (Higgs-shaped 11M x 28, log-loss, population 4096) and C5 (Year-shaped 1M x 90, RMSE,
