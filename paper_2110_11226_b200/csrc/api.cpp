@@ -129,7 +129,12 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   const int g_max = 128;
   pl.xsmem = (size_t)n_cols * tile * sizeof(float) <= 96 * 1024;
   const int occ_guess = 4;
-  const int64_t target = (int64_t)sm_count(device) * occ_guess * 8;
+  // work items per resident CTA slot (tuning knob GP_ITEMS_PER_SLOT)
+  static const int per_slot = [] {
+    const char* e = getenv("GP_ITEMS_PER_SLOT");
+    return e && atoi(e) > 0 ? atoi(e) : 8;
+  }();
+  const int64_t target = (int64_t)sm_count(device) * occ_guess * per_slot;
   const int64_t want_groups = std::max<int64_t>(1, (target + n_tiles - 1) / n_tiles);
   const int G = (int)std::min<int64_t>(g_max, std::max<int64_t>(1, (n_programs + want_groups - 1) / want_groups));
   const int n_groups = (n_programs + G - 1) / G;
@@ -147,7 +152,9 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   return pl;
 }
 
-static const EvalVariant& variant(int v) {
+static const EvalVariant& variant(int v, bool global_x = false) {
+  if (global_x && v == 0) return eval_variant_w4();
+  if (global_x && v == 1) return eval_variant_w8();
   switch (v) {
     case 0: return eval_variant_s4();
     case 1: return eval_variant_s8();
@@ -169,7 +176,9 @@ static gp_status launch_variants(gp_context* ctx, EvalArgs a, const EvalPlan& pl
   }
   for (int v = 0; v < kNumVariants; ++v) {
     if (v > 0 && kVariantStack[v - 1] >= max_stack) break;
-    const EvalVariant& var = variant(v);
+    const EvalVariant& var = variant(v, !pl.xsmem);
+    if (var.shape.SUB != variant(v).shape.SUB)   // the pack kernel laid out SUB copies per program
+      return ctx->fail(GP_ERR_ARG, "evaluator variant %d: wide shape SUB mismatch", v);
     a.stream = (const uint4*)ctx->codestream.p;
     a.gstart = (const int64_t*)ctx->gstart.p + (int64_t)v * (n + 1);
     a.prog_ids = (const int32_t*)ctx->lists.p + (int64_t)v * n;

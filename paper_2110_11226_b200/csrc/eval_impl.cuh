@@ -43,7 +43,16 @@
 
 #define GP_CAT2(a, b) a##b
 #define GP_CAT(a, b) GP_CAT2(a, b)
+// GP_GLOBAL_X_ONLY: a translation unit holding only the global-memory-X instantiations (wide
+// datasets), with its own shape; its variant is eval_variant_w<STACK> (namespace w<STACK>).
+#ifdef GP_GLOBAL_X_ONLY
+#define GP_NS GP_CAT(w, GP_STACK)
+#else
 #define GP_NS GP_CAT(s, GP_STACK)
+#endif
+#ifndef GP_MINB_GLOBAL
+#define GP_MINB_GLOBAL (GP_MINB > 1 ? GP_MINB - 1 : 1)  // global-X path: more live addresses
+#endif
 
 namespace gpb {
 namespace GP_NS {
@@ -202,7 +211,7 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 
 template <bool PREDICT, bool XSMEM>
 // the global-X instantiation holds more live addresses: one resident CTA less
-__global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : (GP_MINB > 1 ? GP_MINB - 1 : 1))
+__global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
     eval_kernel(const EvalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_item;
@@ -450,8 +459,13 @@ static cudaError_t launch_t(const EvalArgs& a, int n_ctas, size_t smem, cudaStre
 
 static cudaError_t launch(const EvalArgs& a, bool predict, bool xsmem, int n_ctas, size_t smem,
                           cudaStream_t s) {
+#ifdef GP_GLOBAL_X_ONLY
+  if (xsmem) return cudaErrorInvalidValue;
+  return predict ? launch_t<true, false>(a, n_ctas, smem, s) : launch_t<false, false>(a, n_ctas, smem, s);
+#else
   if (predict) return xsmem ? launch_t<true, true>(a, n_ctas, smem, s) : launch_t<true, false>(a, n_ctas, smem, s);
   return xsmem ? launch_t<false, true>(a, n_ctas, smem, s) : launch_t<false, false>(a, n_ctas, smem, s);
+#endif
 }
 
 template <bool P, bool XS>
@@ -462,8 +476,13 @@ static int occ_t(size_t smem) {
   return n;
 }
 static int occupancy(bool predict, bool xsmem, size_t smem) {
+#ifdef GP_GLOBAL_X_ONLY
+  if (xsmem) return 0;
+  return predict ? occ_t<true, false>(smem) : occ_t<false, false>(smem);
+#else
   if (predict) return xsmem ? occ_t<true, true>(smem) : occ_t<true, false>(smem);
   return xsmem ? occ_t<false, true>(smem) : occ_t<false, false>(smem);
+#endif
 }
 
 }  // namespace GP_NS

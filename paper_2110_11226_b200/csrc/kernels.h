@@ -86,5 +86,9 @@ const EvalVariant& eval_variant_s4();
 const EvalVariant& eval_variant_s8();
 const EvalVariant& eval_variant_s12();
 const EvalVariant& eval_variant_s20();
+// Wide-dataset shapes of the 4- and 8-slot variants (global-memory X only; eval_w4.cu,
+// eval_w8.cu): same SUB as s4 / s8, so the packed code streams serve both.
+const EvalVariant& eval_variant_w4();
+const EvalVariant& eval_variant_w8();
 
 }  // namespace gpb

@@ -163,12 +163,32 @@ def test_predict_deep_random_all_ops_stress(gp, ctx, orc):
 
 def test_predict_global_x_path(gp, ctx, orc):
     # 28 columns x 2048-row tile exceeds the shared-memory X budget -> per-node L1/L2 loads
+    # (wide-data shapes w4 / w8: 256-thread CTAs, 8 / 4 rows per thread)
     X, _ = synth.higgs_like(2048 * 2 + 301, seed=4)
     nodes, off = synth.random_population(60, seed=9, depth=(1, 6), funcs=synth.ALL_FUNCS,
                                          n_features=28, max_stack=8)
     out, st = ctx.predict(dev(nodes), dev(off), dev(X), max_stack=8)
     torch.cuda.synchronize()
     check_rows(orc, nodes, off, X, out.cpu().numpy())
+
+
+def test_predict_global_x_every_variant(gp, ctx, orc):
+    """Left-deep programs needing 2..20 slots on a wide dataset: every global-X variant (w4, w8,
+    s12, s20) runs, each with its own shape."""
+    X, _ = synth.higgs_like(2048 + 517, seed=6)
+    dn, do = synth.deep_population(60, seed=21, need=(2, 20))
+    dn = dn.copy()
+    v = dn[:, 0] == synth.VAR
+    dn[v, 1] = dn[v, 1] % X.shape[0] + (np.arange(int(v.sum())) % 7)   # spread over columns
+    dn[v, 1] %= X.shape[0]
+    ctx.set_eval_order(False)                  # keep the deep reverse-prefix needs
+    try:
+        out, st = ctx.predict(dev(dn), dev(do), dev(X), max_stack=20)
+    finally:
+        ctx.set_eval_order(True)
+    torch.cuda.synchronize()
+    assert (st.cpu().numpy() == 0).all()
+    check_rows(orc, dn, do, X, out.cpu().numpy())
 
 
 def test_pagie_program_exact(gp, ctx, orc):
