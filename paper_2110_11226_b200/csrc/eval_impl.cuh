@@ -163,38 +163,44 @@ __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
   case LBL(opv_un(OP, UV_C), s): { const float v = apply1<OP>(GP_CONST(cw.y));                 \
     GP_ROWS(st[s][r] = v) } break;
 
-#define GP_EACH_BIN(M, s)                                                                      \
-  M(GP_OP_ADD, s) M(GP_OP_SUB, s) M(GP_OP_MUL, s) M(GP_OP_DIV, s) M(GP_OP_MIN, s)              \
-  M(GP_OP_MAX, s) M(GP_OP_POW, s)
-#define GP_EACH_UN(M, s)                                                                       \
-  M(GP_OP_SIN, s) M(GP_OP_COS, s) M(GP_OP_TAN, s) M(GP_OP_ABS, s) M(GP_OP_NEG, s)              \
-  M(GP_OP_SQRT, s) M(GP_OP_LOG, s) M(GP_OP_EXP, s) M(GP_OP_INV, s) M(GP_OP_SQUARE, s)          \
-  M(GP_OP_CUBE, s) M(GP_OP_TANH, s) M(GP_OP_SINH, s) M(GP_OP_COSH, s) M(GP_OP_ASIN, s)         \
-  M(GP_OP_ACOS, s) M(GP_OP_ATAN, s)
-// every case whose destination slot is s (SS needs slot s + 1 as well)
-#define GP_SLOT_TU(s) GP_PUSH(s) GP_EACH_BIN(GP_BIN_T, s) GP_EACH_UN(GP_UN, s)
-#define GP_SLOT_B(s) GP_EACH_BIN(GP_BIN_SS, s)   // SS and SSR
+// Every case whose destination slot is s (SS needs slot s + 1 as well), listed as the paper's
+// function set (Table 2 / 6: add, sub, mul, div, sin, cos, tan) and the rest of the
+// catalog. (Emitting the paper-set cases of all slots first, as one contiguous code block, was
+// measured: no difference.)
+#define GP_HOT_BIN(M, s) M(GP_OP_ADD, s) M(GP_OP_SUB, s) M(GP_OP_MUL, s) M(GP_OP_DIV, s)
+#define GP_COLD_BIN(M, s) M(GP_OP_MIN, s) M(GP_OP_MAX, s) M(GP_OP_POW, s)
+#define GP_HOT_UN(M, s) M(GP_OP_SIN, s) M(GP_OP_COS, s) M(GP_OP_TAN, s)
+#define GP_COLD_UN(M, s)                                                                       \
+  M(GP_OP_ABS, s) M(GP_OP_NEG, s) M(GP_OP_SQRT, s) M(GP_OP_LOG, s) M(GP_OP_EXP, s)              \
+  M(GP_OP_INV, s) M(GP_OP_SQUARE, s) M(GP_OP_CUBE, s) M(GP_OP_TANH, s) M(GP_OP_SINH, s)         \
+  M(GP_OP_COSH, s) M(GP_OP_ASIN, s) M(GP_OP_ACOS, s) M(GP_OP_ATAN, s)
+#define GP_SLOT_TU_HOT(s) GP_PUSH(s) GP_HOT_BIN(GP_BIN_T, s) GP_HOT_UN(GP_UN, s)
+#define GP_SLOT_TU_COLD(s) GP_COLD_BIN(GP_BIN_T, s) GP_COLD_UN(GP_UN, s)
+#define GP_SLOT_B_HOT(s) GP_HOT_BIN(GP_BIN_SS, s)    // SS and SSR
+#define GP_SLOT_B_COLD(s) GP_COLD_BIN(GP_BIN_SS, s)
+#define GP_SLOT_TU(s) GP_SLOT_TU_HOT(s) GP_SLOT_TU_COLD(s)
+#define GP_SLOT_B(s) GP_SLOT_B_HOT(s) GP_SLOT_B_COLD(s)
 
 #define GP_FOR_0_2(M) M(0) M(1) M(2)
 #define GP_FOR_0_6(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6)
 #define GP_FOR_8_10(M) M(8) M(9) M(10)
 #define GP_FOR_12_18(M) M(12) M(13) M(14) M(15) M(16) M(17) M(18)
+// GP_CASES(TU, B): the TU cases of every slot, then the SS / SSR cases of every slot below the top
 #if GP_STACK == 4
-#define GP_ALL_CASES GP_FOR_0_2(GP_SLOT_TU) GP_SLOT_TU(3) GP_FOR_0_2(GP_SLOT_B)
+#define GP_CASES(TU, B) GP_FOR_0_2(TU) TU(3) GP_FOR_0_2(B)
 #elif GP_STACK == 8
-#define GP_ALL_CASES GP_FOR_0_6(GP_SLOT_TU) GP_SLOT_TU(7) GP_FOR_0_6(GP_SLOT_B)
+#define GP_CASES(TU, B) GP_FOR_0_6(TU) TU(7) GP_FOR_0_6(B)
 #elif GP_STACK == 12
-#define GP_ALL_CASES                                                                           \
-  GP_FOR_0_6(GP_SLOT_TU) GP_SLOT_TU(7) GP_FOR_8_10(GP_SLOT_TU) GP_SLOT_TU(11)                  \
-  GP_FOR_0_6(GP_SLOT_B) GP_SLOT_B(7) GP_FOR_8_10(GP_SLOT_B)
+#define GP_CASES(TU, B)                                                                        \
+  GP_FOR_0_6(TU) TU(7) GP_FOR_8_10(TU) TU(11) GP_FOR_0_6(B) B(7) GP_FOR_8_10(B)
 #elif GP_STACK == 20
-#define GP_ALL_CASES                                                                           \
-  GP_FOR_0_6(GP_SLOT_TU) GP_SLOT_TU(7) GP_FOR_8_10(GP_SLOT_TU) GP_SLOT_TU(11)                  \
-  GP_FOR_12_18(GP_SLOT_TU) GP_SLOT_TU(19)                                                      \
-  GP_FOR_0_6(GP_SLOT_B) GP_SLOT_B(7) GP_FOR_8_10(GP_SLOT_B) GP_SLOT_B(11) GP_FOR_12_18(GP_SLOT_B)
+#define GP_CASES(TU, B)                                                                        \
+  GP_FOR_0_6(TU) TU(7) GP_FOR_8_10(TU) TU(11) GP_FOR_12_18(TU) TU(19)                          \
+  GP_FOR_0_6(B) B(7) GP_FOR_8_10(B) B(11) GP_FOR_12_18(B)
 #else
 #error "GP_STACK must be 4, 8, 12 or 20"
 #endif
+#define GP_ALL_CASES GP_CASES(GP_SLOT_TU, GP_SLOT_B)
 
 template <int M> struct MTag { static constexpr int value = M; };
 

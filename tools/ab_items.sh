@@ -1,7 +1,7 @@
 #!/bin/bash
-# Work-item granularity sweep (GP_ITEMS_PER_SLOT) on C3 and C5.
-for k in 8 16 32; do
-  for c in c3 c5; do
+# Work-item granularity sweep (GP_ITEMS_PER_SLOT) on C3 and C5 ($ITEMS, default "8 16 32").
+for k in ${ITEMS:-8 16 32}; do
+  for c in ${CONFIGS:-c3 c5}; do
     line=$(GP_ITEMS_PER_SLOT=$k timeout 400 python bench.py --config $c --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1)
     echo "$line" > gpurun_out/abi_${k}_$c.json
     echo "items/slot $k $c | $(echo $line | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"]/1e12,3), "Tnode/s", round(d["ms_per_step"],2), "ms", "frac", d["roofline"]["frac"], "gen0", d["roofline_gen0"]["frac"])')"

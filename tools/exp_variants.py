@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Builds alternative evaluator shapes for an A/B on one GPU box (tools/ab_libs.sh).
 
-    python tools/exp_variants.py s4 name=NT,R,SUB,MINB,RED_ROWS[,Y_REGS] [name=...]
+    python tools/exp_variants.py s4 name=NT,R,SUB,MINB,RED_ROWS[,Y_REGS[,MACRO:VALUE...]] [name=...]
 
 Each experiment recompiles ONE variant translation unit (eval_<v>.cu's shape macros replaced)
 and links it with the in-tree objects of everything else into
@@ -23,13 +23,14 @@ STACK = {"s4": 4, "s8": 8, "s12": 12, "s20": 20}
 def one(var, name, shape):
     nt, r, sub, minb, rr, *extra = shape.split(",")
     yregs = extra[0] if extra else "0"
+    defs = "".join(f"#define {kv.split(':')[0]} {kv.split(':')[1]}\n" for kv in extra[1:])
     exp = os.path.join(PKG, "_exp")
     os.makedirs(exp, exist_ok=True)
     src = os.path.join(exp, f"eval_{var}_{name}.cu")
     with open(src, "w") as f:
         f.write(f"#define GP_STACK {STACK[var]}\n#define GP_R {r}\n#define GP_SUB {sub}\n"
                 f"#define GP_NT {nt}\n#define GP_MINB {minb}\n#define GP_RED_ROWS {rr}\n"
-                f"#define GP_Y_REGS {yregs}\n"
+                f"#define GP_Y_REGS {yregs}\n" + defs +
                 f'#include "{os.path.join(PKG, "csrc", "eval_impl.cuh")}"\n')
     obj = src + ".o"
     impl = os.path.join(PKG, "csrc", "eval_impl.cuh")
