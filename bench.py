@@ -133,7 +133,7 @@ def algorithmic_ops(op_count, rows, metric, n_programs, const_programs=0):
     return sfu, fp32
 
 
-def roofline_of(sfu, fp32, eval_ms, launches, step_ms):
+def roofline_of(sfu, fp32, eval_ms, launches, step_ms, traffic=True):
     """Binding ALU pipe of the evaluator for the given algorithmic work: SFU (MUFU) or FP32."""
     eval_s = eval_ms * 1e-3
     f_sfu, f_fp32 = sfu / eval_s / SFU_PEAK, fp32 / eval_s / FP32_PEAK
@@ -143,8 +143,9 @@ def roofline_of(sfu, fp32, eval_ms, launches, step_ms):
     else:
         r = {"bound": "alu", "pipe": "FP32", "achieved": round(fp32 / eval_s / 1e12, 4),
              "peak": round(FP32_PEAK / 1e12, 4), "unit": "TFLOP/s (fp32)", "frac": round(f_fp32, 4)}
-    r.update({"traffic": ncu_traffic(), "traffic_scope": "DRAM bytes of one evaluation's eval "
-              "launches (profiles/eval_kernel_ncu.json)", "sfu_frac": round(f_sfu, 4), "fp32_frac": round(f_fp32, 4),
+    r.update({"traffic": ncu_traffic() if traffic else None,
+              "traffic_scope": "DRAM bytes of one C3 evaluation's eval launches "
+                               "(profiles/eval_kernel_ncu.json)" if traffic else "measured for C3 only", "sfu_frac": round(f_sfu, 4), "fp32_frac": round(f_fp32, 4),
               "eval_ms_per_launch": round(eval_ms / max(launches, 1), 3),
               "eval_share_of_step": round(eval_ms / step_ms, 4),
               "peak_note": "SFU: 148 SMs x 16 MUFU/clk x 1965 MHz (measured MUFU.SIN 4.63e12/s); "
@@ -262,7 +263,7 @@ def run_b200(args, cfg):
         a, b2 = algorithmic_ops(s["op_count"], rows_local, cfg["metric"], cfg["pop"],
                                 0 if args.no_const_programs else s["const_programs"])
         sfu, fp32 = sfu + a, fp32 + b2
-    roofline = roofline_of(sfu, fp32, eval_ms, eval_launches, ms)
+    roofline = roofline_of(sfu, fp32, eval_ms, eval_launches, ms, traffic=args.config == "c3")
     var_nodes = sum(sum(s["op_count"]) for s in steps) * m_global
     const_share = float(np.mean([s["const_nodes"] / max(1, s["total_nodes"]) for s in steps]))
 
@@ -286,7 +287,7 @@ def run_b200(args, cfg):
         ctx.set_profiling(False)
         a0, b0 = algorithmic_ops(ops0, rows_local, cfg["metric"], cfg["pop"],
                                  0 if args.no_const_programs else cp0)
-        roof0 = roofline_of(a0 * reps, b0 * reps, ms0, l0, ms0)
+        roof0 = roofline_of(a0 * reps, b0 * reps, ms0, l0, ms0, traffic=args.config == "c3")
         roof0["node_evals_per_s"] = float(len(n0)) * rows_local * reps / (ms0 * 1e-3)
         roof0["population"] = "generation 0 (ramped half-and-half), mean length %.2f" % (
             len(n0) / (len(o0) - 1))
