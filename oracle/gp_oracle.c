@@ -143,6 +143,7 @@ int orc_stack_need(const onode* nodes, int64_t len) {
 #define SFU_ABS (3.5762786865234375e-07)  /* 2^-21.41 ~ 3.6e-7: MUFU sin/cos/lg2 absolute budget */
 #define CLAMP_BIG 1e30
 #define PROT 1e-3
+#define FTZ_IN(v) (fabs(v) < (double)FLT_MIN ? fabs(v) : 0.0)
 
 typedef struct { double v, e; int flags; } oval;
 
@@ -197,8 +198,9 @@ static oval eval_rec(const onode* nodes, int64_t* i, const float* X, int64_t ld,
   onode n = nodes[*i];
   *i += 1;
   oval r = {0.0, 0.0, 0};
-  if (n.op == O_VAR) { r.v = (double)X[(int64_t)n.payload * ld + row]; return r; }
-  if (n.op == O_CONST) { r.v = (double)payload_f(n.payload); return r; }
+  /* a subnormal fp32 input is flushed to zero by an FTZ evaluation: error |v| < FLT_MIN */
+  if (n.op == O_VAR) { r.v = (double)X[(int64_t)n.payload * ld + row]; r.e = FTZ_IN(r.v); return r; }
+  if (n.op == O_CONST) { r.v = (double)payload_f(n.payload); r.e = FTZ_IN(r.v); return r; }
   int ar = orc_arity(n.op);
   oval A = eval_rec(nodes, i, X, ld, row);
   oval B = {0.0, 0.0, 0};
@@ -276,6 +278,10 @@ static oval eval_rec(const onode* nodes, int64_t* i, const float* X, int64_t ld,
       break;
     }
   }
+  /* underflow: an fp32 result below FLT_MIN is subnormal (IEEE, absolute error <= 2^-150) or
+   * flushed to zero (FTZ evaluation, error < FLT_MIN); the relative budgets above do not cover
+   * either, so every function result carries an absolute FLT_MIN term */
+  r.e += (double)FLT_MIN;
   if (!isfinite(v) || av > (double)FLT_MAX) r.flags |= 1;
   if (isnan(r.e)) r.e = INFINITY;   /* an undefined first-order bound is "unbounded" */
   return r;
@@ -342,10 +348,26 @@ void orc_rank_vector(const double* v, int64_t n, double* ranks) {
   free(t);
 }
 
+/* 1 if v takes one value on every live row (w != 0): zero variance exactly. The rounded
+ * weighted mean of equal values need not equal them, so this is decided on the values. */
+static int live_constant(const double* v, const float* w, int64_t n) {
+  int64_t first = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    if ((w ? (double)w[i] : 1.0) == 0.0) continue;
+    if (first < 0) first = i;
+    else if (!(v[i] == v[first])) return 0;
+  }
+  return 1;
+}
+
 /* weighted Pearson correlation of a and b: weighted means first, then centred sums
  * (two-pass); w == 0 rows skipped; zero variance or non-finite r -> 0 and *undefined = 1. */
 static double pearson_w(const double* a, const double* b, const float* w, int64_t n, double W,
                         int* undefined) {
+  if (live_constant(a, w, n) || live_constant(b, w, n)) {
+    if (undefined) *undefined = 1;
+    return 0.0;
+  }
   double ma = 0.0, mb = 0.0;
   for (int64_t i = 0; i < n; ++i) {
     double wi = w ? (double)w[i] : 1.0;
@@ -418,7 +440,13 @@ double orc_fitness(int metric, const double* yh, const float* y, const float* w,
     if (!isfinite(f)) f = INFINITY;
     return f;
   }
-  /* Pearson: weighted means first, then centred sums (two-pass). */
+  /* Pearson: weighted means first, then centred sums (two-pass). A prediction that
+   * is the same value on every live row has zero variance exactly (S:202 ConstantVector): the
+   * rounded mean of equal values need not equal them, so this is decided on the values. */
+  if (live_constant(yh, w, n)) {
+    if (undefined) *undefined = 1;
+    return 0.0;
+  }
   double my = 0.0, mh = 0.0;
   for (int64_t i = 0; i < n; ++i) {
     double wi = w ? (double)w[i] : 1.0;
@@ -475,7 +503,8 @@ double orc_fitness_sensitivity(int metric, const double* yh, const double* E, co
   /* Spearman: ranks change by whole steps, no first-order bound (tests use exactly representable
    * inputs or a rank-swap tolerance) */
   if (metric == 5) return 0.0;
-  /* Pearson: |dr/dyh_i| = w_i |(y_i - my)/sqrt(sxx syy) - r (yh_i - mh)/sxx| */
+  /* Pearson: |dr/dyh_i| = w_i |(y_i - my)/sqrt(sxx syy) - r (yh_i - mh)/sxx|, bounded by the sum
+   * of the two magnitudes */
   double my = 0.0, mh = 0.0;
   for (int64_t i = 0; i < n; ++i) {
     double wi = w ? (double)w[i] : 1.0;
@@ -499,10 +528,13 @@ double orc_fitness_sensitivity(int metric, const double* yh, const double* E, co
   for (int64_t i = 0; i < n; ++i) {
     double wi = w ? (double)w[i] : 1.0;
     if (wi == 0.0) continue;
-    double g = fabs(((double)y[i] - my) / sqrt(sxx * syy) - r * (yh[i] - mh) / sxx);
+    /* triangle inequality instead of the difference: the two terms can cancel to far below
+     * their rounding error (outliers near the 1e30 clamps), which would understate the bound */
+    double g = fabs((double)y[i] - my) / sqrt(sxx * syy) + fabs(r) * fabs(yh[i] - mh) / sxx;
     s += wi * g * E[i];
   }
-  if (!(s <= 2.0)) s = 2.0;   /* r lies in [-1, 1] */
+  /* r lies in [-1, 1]: a bound of 2 or more says nothing (no usable first-order bound) */
+  if (!(s < 2.0)) s = INFINITY;
   return s;
 }
 

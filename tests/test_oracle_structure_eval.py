@@ -230,39 +230,157 @@ def test_recursive_equals_stack_walk(orc):
 
 
 # ---- the error bound E: an fp32 evaluation with IEEE-accurate ops must land within E ------------
-def _f32_eval(orc, prog, row):
-    """fp32 emulation (numpy float32, correctly rounded +-*/; float32 libm for the rest)."""
-    f = np.float32
+_F = np.float32
+_FLT_MIN = float(np.finfo(np.float32).tiny)
+
+
+def _ftz(x, on):
+    """Flush-to-zero of an fp32 value (the GPU build's -ftz=true): subnormals become signed 0."""
+    return _F(0.0) * np.sign(x) if on and abs(x) < _FLT_MIN else x
+
+
+def _f32_op(op, a, b):
+    """One catalog function in fp32 (S:117-122, S:132 protected rules; C2): the IEEE
+    ops correctly rounded by numpy float32, the others as the double libm value rounded to fp32
+    (within an ulp of the exact value -- the evaluator's budgets are wider)."""
+    T, BIG = _F(1e-3), _F(1e30)
+    d = lambda v: _F(v)                                      # noqa: E731 (round double -> fp32)
+    A, B = float(a), float(b)
+    with np.errstate(all="ignore"):
+        if op == 2: return a + b
+        if op == 3: return a - b
+        if op == 4: return a * b
+        if op == 5: return _F(1) if abs(b) < T else a / b
+        if op == 6: return np.fmin(a, b)
+        if op == 7: return np.fmax(a, b)
+        if op == 8:
+            if b == 0: return _F(1)
+            if a == 0: return _F(0) if b > 0 else BIG
+            lg = B * math.log(abs(A))
+            return min(d(math.exp(lg)) if lg < 89.0 else _F(np.inf), BIG)
+        if op == 9: return d(math.sin(A))
+        if op == 10: return d(math.cos(A))
+        if op == 11: return d(math.tan(A))
+        if op == 12: return abs(a)
+        if op == 13: return -a
+        if op == 14: return d(math.sqrt(abs(A)))
+        if op == 15: return _F(0) if abs(a) < T else d(math.log(abs(A)))
+        if op == 16: return min(d(math.exp(A)) if A < 89 else _F(np.inf), BIG)
+        if op == 17: return _F(1) if abs(a) < T else _F(1) / a
+        if op == 18: return a * a
+        if op == 19: return (a * a) * a
+        if op == 20: return d(math.tanh(A))
+        if op == 21: return max(min(d(math.sinh(A)) if abs(A) < 89 else _F(math.copysign(np.inf, A)), BIG), -BIG)
+        if op == 22: return min(d(math.cosh(A)) if abs(A) < 89 else _F(np.inf), BIG)
+        if op == 23: return d(math.asin(min(max(A, -1.0), 1.0)))
+        if op == 24: return d(math.acos(min(max(A, -1.0), 1.0)))
+        if op == 25: return d(math.atan(A))
+    raise ValueError(op)
+
+
+def _f32_eval(orc, prog, row, ftz=False):
+    """fp32 emulation of a program by a reverse-prefix stack walk (an independent evaluation
+    order from the oracle's recursion), optionally flushing subnormals like the GPU build."""
     st = []
-    T = f(1e-3)
     for op, pl in reversed([tuple(t) for t in prog]):
         if op == 0:
-            st.append(f(row[pl]))
+            st.append(_ftz(_F(row[pl]), ftz))
             continue
         if op == 1:
-            st.append(f(orc.bits_f32(pl)))
+            st.append(_ftz(_F(orc.bits_f32(pl)), ftz))
             continue
         a = st.pop()
-        b = st.pop() if orc.arity(op) == 2 else f(0)
-        with np.errstate(all="ignore"):
-            r = {2: lambda: a + b, 3: lambda: a - b, 4: lambda: a * b,
-                 5: lambda: f(1) if abs(b) < T else a / b, 9: lambda: np.sin(a),
-                 10: lambda: np.cos(a), 11: lambda: np.tan(a)}[op]()
-        st.append(f(r))
+        b = st.pop() if orc.arity(op) == 2 else _F(0)
+        st.append(_ftz(_F(_f32_op(op, a, b)), ftz))
     return st[0]
 
 
-def test_error_bound_covers_fp32_evaluation(orc):
-    nodes, off = synth.random_population(300, seed=21, depth=(1, 7))
-    X, _ = synth.pagie_grid(8)
+def _bound_rows(n=48, seed=5):
+    """Rows for the E pins: the Pagie grid plus values over many magnitudes (1e-20 .. 1e3, both
+    signs), so underflow (cube, pow, mul of tiny values), overflow and the protected thresholds
+    are all reached."""
+    Xg, _ = synth.pagie_grid(6)
+    rng = np.random.default_rng(seed)
+    mag = 10.0 ** rng.uniform(-20, 3, (2, n))
+    Xr = (mag * rng.choice([-1.0, 1.0], (2, n))).astype(np.float32)
+    return np.ascontiguousarray(np.concatenate([Xg, Xr], axis=1))
+
+
+@pytest.mark.parametrize("funcs,seed", [(synth.TABLE2_SET, 21), (synth.ALL_FUNCS, 22),
+                                        (synth.ALL_FUNCS, 23)])
+def test_error_bound_covers_fp32_evaluation(orc, funcs, seed):
+    """SURVEY "exact result within the error bound": for every one of the 24 catalog functions an
+    fp32 evaluation (IEEE with gradual underflow, and flush-to-zero as on the GPU) lies within the
+    oracle's E of the exact (double) value on every row the oracle does not flag."""
+    nodes, off = synth.random_population(260, seed=seed, depth=(1, 6), funcs=funcs)
+    X = _bound_rows()
     checked = 0
+    used = set()
     for i in range(len(off) - 1):
         p = nodes[off[i]:off[i + 1]]
         v, e, fl = orc.eval_program(p, X)
         for r in range(X.shape[1]):
-            if fl[r]:
+            if fl[r] or not math.isfinite(e[r]):
                 continue
-            g = float(_f32_eval(orc, p, X[:, r]))
-            assert abs(g - v[r]) <= e[r] + 1e-300, (i, r, g, v[r], e[r])
+            for ftz in (False, True):
+                g = float(_f32_eval(orc, p, X[:, r], ftz))
+                assert abs(g - v[r]) <= e[r], (i, r, ftz, g, v[r], e[r], p.tolist())
             checked += 1
+        used.update(int(o) for o in p[:, 0] if o > 1)
     assert checked > 10_000
+    assert used == set(funcs)
+
+
+def test_error_bound_underflow_cases(orc):
+    """Results below FLT_MIN: fp32 gives a subnormal or (FTZ) zero where double keeps 1e-60; E must
+    cover the difference (the round-1 review found cube / pow rows violating E without an
+    underflow term)."""
+    x = ("var", 0)
+    X = np.array([[1e-20, -3e-13, 2e-30]], np.float32)
+    for prog in (P(orc, "cube", x), P(orc, "mul", x, x), P(orc, "square", x),
+                 P(orc, "pow", x, ("const", 3.0)), P(orc, "mul", "cube", x, ("const", 0.5))):
+        v, e, fl = orc.eval_program(prog, X)
+        for r in range(X.shape[1]):
+            assert not fl[r]
+            for ftz in (False, True):
+                g = float(_f32_eval(orc, prog, X[:, r], ftz))
+                assert abs(g - v[r]) <= e[r], (prog.tolist(), r, g, v[r], e[r])
+        assert (e >= np.abs(v)).all() or (np.abs(v) >= _FLT_MIN).any()
+
+
+@pytest.mark.parametrize("metric", ["mae", "mse", "rmse", "logloss", "pearson"])
+def test_fitness_sensitivity_covers_fp32_fitness(orc, metric):
+    """orc_fitness_sensitivity pin (SURVEY acceptance rule per program): the fitness of the fp32
+    predictions (each within E of the exact one) lies within the sensitivity of the exact fitness
+    -- brute force over random programs, with the fitness itself from the oracle's metric on the
+    fp32 values. Also: predictions perturbed by +-E on every row (signs random) stay within
+    the bound to first order (factor 2 slack for the second-order term)."""
+    X = _bound_rows(n=24, seed=9)[:, :60]
+    if metric == "logloss":
+        y = (X[0] > 0).astype(np.float32)
+    else:
+        y = np.asarray([orc.pagie(float(a), float(b)) for a, b in X.T], np.float32)
+    w = synth.weights(X.shape[1], seed=3)
+    nodes, off = synth.random_population(120, seed=31, depth=(1, 5), funcs=synth.ALL_FUNCS)
+    rng = np.random.default_rng(4)
+    checked = 0
+    for i in range(len(off) - 1):
+        p = nodes[off[i]:off[i + 1]]
+        v, e, fl = orc.eval_program(p, X)
+        live = w != 0
+        if fl[live].any() or not np.isfinite(e[live]).all() or np.ptp(v[live]) == 0:
+            continue
+        F = orc.fitness(metric, v, y, w)[0]
+        s = orc.fitness_sensitivity(metric, v, e, y, w)
+        if not math.isfinite(s) or not math.isfinite(F):
+            continue
+        g = np.array([float(_f32_eval(orc, p, X[:, r], True)) for r in range(X.shape[1])])
+        Fg = orc.fitness(metric, g, y, w)[0]
+        # (+ double rounding of the metric's own sums, ~1e-16 relative)
+        assert abs(Fg - F) <= s * (1 + 1e-9) + 1e-12 * abs(F) + 1e-15, (i, metric, Fg, F, s)
+        for _ in range(3):
+            vp = v + e * rng.choice([-1.0, 1.0], v.shape)
+            Fp = orc.fitness(metric, vp, y, w)[0]
+            assert abs(Fp - F) <= 2 * s + 1e-12 * abs(F), (i, metric, Fp, F, s)
+        checked += 1
+    assert checked >= 40
