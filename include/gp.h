@@ -122,12 +122,16 @@ gp_status gp_get_unique_id(void* out_id);
 gp_status gp_context_create(gp_context** out, int device, void* stream, const void* nccl_unique_id,
                             int rank, int world_size);
 gp_status gp_context_destroy(gp_context* ctx);
+/* Switches the context's stream. Work already queued on the old stream is waited for first
+ * (the context's buffers may be reallocated on the new stream). */
 gp_status gp_context_set_stream(gp_context* ctx, void* stream);
 
 /* Pearson's single-pass evaluation accumulates about a per-program shift K_p = f_p(x_ref)
  * (C9). All ranks must use the same reference row: pass the GLOBAL first row
  * x_ref [host, n_cols floats] and its label y_ref. If never called, the first row of the X / y
- * passed to gp_evaluate is used (correct for world_size == 1). */
+ * passed to gp_evaluate is used; on a row-sharded communicator rank 0's first row is broadcast
+ * to every rank inside gp_evaluate (one ncclBroadcast of n_cols + 1 floats), so the shifts
+ * always agree. gp_evaluate_partial without a communicator cannot do that: set the row. */
 gp_status gp_context_set_reference_row(gp_context* ctx, const float* x_ref, int32_t n_cols,
                                        float y_ref);
 
@@ -162,6 +166,15 @@ gp_status gp_context_set_const_programs(gp_context* ctx, int closed_form);
  * Results are identical on every rank in both modes. */
 typedef enum { GP_SHARD_ROWS = 0, GP_SHARD_PROGRAMS = 1 } gp_shard;
 gp_status gp_context_set_shard(gp_context* ctx, gp_shard mode);
+/* Work decomposition override (tests and tuning): group_size programs per work item
+ * (1..128, 0 = automatic) and tiles_per_chunk row tiles of 2048 rows per work item (0 =
+ * automatic). Only the fp64 summation order of the per-chunk partial sums depends on it. */
+gp_status gp_context_set_plan(gp_context* ctx, int32_t group_size, int64_t tiles_per_chunk);
+/* Restricts gp_evaluate / gp_evaluate_partial to the programs [lo, hi) (hi < 0: all) -- the
+ * per-rank program chunk of GP_SHARD_PROGRAMS, usable without a communicator (a caller that
+ * distributes programs itself, and the single-GPU simulation of that mode). Fitness and status of
+ * the programs outside the range are unspecified. */
+gp_status gp_context_set_program_range(gp_context* ctx, int32_t lo, int32_t hi);
 /* Number of CUDA kernels this context has launched (all entry points) since the last reset. */
 gp_status gp_context_kernel_launches(gp_context* ctx, int64_t* launches, int reset);
 
@@ -201,6 +214,32 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
                       int32_t n_programs, int64_t n_nodes, int32_t max_stack, const float* X,
                       int64_t ldx, const float* y, const float* w, int64_t n_rows, int32_t n_cols,
                       gp_metric metric, float* fitness_out, uint32_t* status_out);
+
+/* gp_evaluate_partial -- the per-rank half of gp_evaluate, before ranks are combined (SURVEY
+ * A2-A5): the fp64 per-program sums of this call's rows,
+ *   sums_out[p S + k], S = 3 for Pearson (S_d, S_dd, S_dy about the shifts K_p, K_y of
+ *                     DESIGN.md C9), else 1 (sum_i w_i loss_i);
+ *   sums_out[n S + 0..2] = W = sum_i w_i, S_y, S_yy (Pearson: about K_y; LogLoss: S_y = weight
+ *                     of the rows with y > 1/2; MSE / RMSE: about 0),
+ * with zeros for programs the evaluator skipped (invalid; variable-free under a closed-form
+ * metric; outside gp_context_set_program_range). Summing the outputs of row shards (any order)
+ * and passing the total to gp_finalize_sums gives what gp_evaluate gives with one row-sharded
+ * communicator -- this is the data flow of the NCCL path with the all-reduce made explicit.
+ * Arguments as gp_evaluate; sums_out [host|device] fp64[n_programs * S + 3]. Spearman is not
+ * additive over rows: GP_ERR_UNSUPPORTED. For Pearson every shard must use the same reference
+ * row (gp_context_set_reference_row). */
+gp_status gp_evaluate_partial(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
+                              int32_t n_programs, int64_t n_nodes, int32_t max_stack,
+                              const float* X, int64_t ldx, const float* y, const float* w,
+                              int64_t n_rows, int32_t n_cols, gp_metric metric, double* sums_out);
+/* gp_finalize_sums -- the other half: fitness and status from sums laid out as
+ * gp_evaluate_partial writes them (summed over shards). The programs are compiled again for
+ * their status bits and the closed-form constants. sums [host|device]; fitness_out / status_out
+ * as gp_evaluate. */
+gp_status gp_finalize_sums(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
+                           int32_t n_programs, int64_t n_nodes, int32_t max_stack, int32_t n_cols,
+                           const double* sums, gp_metric metric, float* fitness_out,
+                           uint32_t* status_out);
 
 /* gp_predict -- the execution step alone ("all programs ... evaluated on the given
  * data-set, to produce set of predicted values"): out[p * ld_out + i] = f_p(x_i) in fp32 for

@@ -175,6 +175,49 @@ class Context:
                                  _ptr(fitness_out), _ptr(status_out)), self.handle, "gp_evaluate")
         return fitness_out, status_out
 
+    def evaluate_partial(self, nodes, offsets, X, y, w=None, metric="mse",
+                         max_stack: int = GP_MAX_STACK, sums_out=None, n_rows: int | None = None):
+        """gp_evaluate_partial: fp64 per-program sums of these rows (program order, S per
+        program, then W, S_y, S_yy). Returns sums_out (float64 on X's device by default)."""
+        import torch
+        n = offsets.shape[0] - 1
+        S = 3 if metric == "pearson" else 1
+        n_rows = X.shape[1] if n_rows is None else n_rows
+        if sums_out is None:
+            sums_out = torch.empty(n * S + 3, dtype=torch.float64, device=X.device)
+        _check(lib().gp_evaluate_partial(self.handle, _ptr(nodes), _ptr(offsets), n,
+                                         int(nodes.shape[0]), int(max_stack), _ptr(X),
+                                         int(X.stride(0)), _ptr(y), _ptr(w), int(n_rows),
+                                         int(X.shape[0]), _metric_id(metric), _ptr(sums_out)),
+               self.handle, "gp_evaluate_partial")
+        return sums_out
+
+    def finalize_sums(self, nodes, offsets, sums, n_cols: int, metric="mse",
+                      max_stack: int = GP_MAX_STACK, fitness_out=None, status_out=None):
+        """gp_finalize_sums: fitness / status from (shard-summed) gp_evaluate_partial sums."""
+        import torch
+        n = offsets.shape[0] - 1
+        dev = sums.device
+        if fitness_out is None:
+            fitness_out = torch.empty(n, dtype=torch.float32, device=dev)
+        if status_out is None:
+            status_out = torch.empty(n, dtype=torch.int32, device=dev)
+        _check(lib().gp_finalize_sums(self.handle, _ptr(nodes), _ptr(offsets), n,
+                                      int(nodes.shape[0]), int(max_stack), int(n_cols), _ptr(sums),
+                                      _metric_id(metric), _ptr(fitness_out), _ptr(status_out)),
+               self.handle, "gp_finalize_sums")
+        return fitness_out, status_out
+
+    def set_plan(self, group_size: int = 0, tiles_per_chunk: int = 0):
+        """gp_context_set_plan (0 = automatic)."""
+        _check(lib().gp_context_set_plan(self.handle, int(group_size), int(tiles_per_chunk)),
+               self.handle, "gp_context_set_plan")
+
+    def set_program_range(self, lo: int = 0, hi: int = -1):
+        """gp_context_set_program_range ([lo, hi); hi < 0 = all)."""
+        _check(lib().gp_context_set_program_range(self.handle, int(lo), int(hi)), self.handle,
+               "gp_context_set_program_range")
+
     def predict(self, nodes, offsets, X, max_stack: int = GP_MAX_STACK, out=None, status_out=None):
         """gp_predict: out[p, i] = f_p(x_i) (float32, device)."""
         import torch

@@ -32,6 +32,11 @@ SIGNATURES = {
     "gp_context_set_shard": ([P, ctypes.c_int], ctypes.c_int),
     "gp_evaluate": ([P, P, P, i32, i64, i32, P, i64, P, P, i64, i32, ctypes.c_int, P, P],
                     ctypes.c_int),
+    "gp_evaluate_partial": ([P, P, P, i32, i64, i32, P, i64, P, P, i64, i32, ctypes.c_int, P],
+                            ctypes.c_int),
+    "gp_finalize_sums": ([P, P, P, i32, i64, i32, i32, P, ctypes.c_int, P, P], ctypes.c_int),
+    "gp_context_set_plan": ([P, i32, i64], ctypes.c_int),
+    "gp_context_set_program_range": ([P, i32, i32], ctypes.c_int),
     "gp_predict": ([P, P, P, i32, i64, i32, P, i64, i64, i32, P, i64, P], ctypes.c_int),
     "gp_tournament_select": ([P, P, P, i32, i32, i32, f32, i32, u64, u32, P], ctypes.c_int),
     "gp_config_default": ([P], None),

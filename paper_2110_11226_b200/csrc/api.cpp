@@ -29,6 +29,8 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi& nccl() {
@@ -43,9 +45,10 @@ NcclApi& nccl() {
       api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
       api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
       api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+      api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
       api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
       api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce &&
-               api.AllGather;
+               api.AllGather && api.Broadcast;
     }
   }
   return api;
@@ -126,7 +129,7 @@ int gpb::sm_count(int device) {
 // keep the persistent CTAs' queue balanced to the end (C3 SFU frac: 0.72 at 8 items per slot,
 // 0.77 at 32, 0.79 at 128). All variants share the 2048-row tile.
 EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t n_cols, int S,
-                        bool predict, bool weighted) {
+                        bool predict, bool weighted, int force_G, int64_t force_tpc) {
   EvalPlan pl;
   const int tile = kTile;
   const int64_t n_tiles = (n_rows + tile - 1) / tile;
@@ -140,10 +143,12 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   }();
   const int64_t slots = (int64_t)sm_count(device) * occ_guess;
   const int64_t want_groups = std::max<int64_t>(1, (slots * 8 + n_tiles - 1) / n_tiles);
-  const int G = (int)std::min<int64_t>(g_max, std::max<int64_t>(1, (n_programs + want_groups - 1) / want_groups));
+  int G = (int)std::min<int64_t>(g_max, std::max<int64_t>(1, (n_programs + want_groups - 1) / want_groups));
+  if (force_G > 0) G = std::min(force_G, g_max);               // gp_context_set_plan
   const int n_groups = (n_programs + G - 1) / G;
   int64_t Q = std::min<int64_t>(n_tiles, std::max<int64_t>(1, (slots * per_slot + n_groups - 1) / n_groups));
-  const int64_t tpc = (n_tiles + Q - 1) / Q;
+  int64_t tpc = (n_tiles + Q - 1) / Q;
+  if (force_tpc > 0) tpc = std::min<int64_t>(force_tpc, n_tiles);
   Q = (n_tiles + tpc - 1) / tpc;
   pl.G = G;
   pl.n_groups = n_groups;
@@ -188,6 +193,7 @@ static gp_status launch_variants(gp_context* ctx, EvalArgs a, const EvalPlan& pl
     a.prog_ids = (const int32_t*)ctx->lists.p + (int64_t)v * n;
     a.prog_count = (const int32_t*)ctx->counts.p + v;
     a.work_counter = (int32_t*)ctx->counts.p + kNumVariants + v;
+    a.part_base = (const int32_t*)ctx->inv.p + n + v;
     const size_t smem = pl.smem + (predict ? 0 : var.acc_bytes(pl.G, a.metric == GP_PEARSON ? 3 : 1));
     const int occ = std::max(1, var.occupancy(predict, pl.xsmem, smem));
     gp_status s = ctx->launch(var.launch(a, predict, pl.xsmem, ctx->sms * occ, smem, ctx->stream),
@@ -282,7 +288,27 @@ gp_status gp_context_destroy(gp_context* ctx) {
 
 gp_status gp_context_set_stream(gp_context* ctx, void* stream) {
   if (!ctx) return GP_ERR_ARG;
+  if ((cudaStream_t)stream == ctx->stream) return GP_OK;
+  // buffers grown later are freed / allocated stream-ordered on the NEW stream: the old stream's
+  // queued work that may still read them must be finished first
+  cudaSetDevice(ctx->device);
+  gp_status s = ctx->cuda(cudaStreamSynchronize(ctx->stream), "set_stream: old stream");
+  if (s) return s;
   ctx->stream = (cudaStream_t)stream;
+  return GP_OK;
+}
+
+gp_status gp_context_set_plan(gp_context* ctx, int32_t group_size, int64_t tiles_per_chunk) {
+  if (!ctx || group_size < 0 || group_size > 128 || tiles_per_chunk < 0) return GP_ERR_ARG;
+  ctx->plan_G = group_size;
+  ctx->plan_tpc = tiles_per_chunk;
+  return GP_OK;
+}
+
+gp_status gp_context_set_program_range(gp_context* ctx, int32_t lo, int32_t hi) {
+  if (!ctx || lo < 0 || (hi >= 0 && hi < lo)) return GP_ERR_ARG;
+  ctx->range_lo = lo;
+  ctx->range_hi = hi;
   return GP_OK;
 }
 
@@ -384,6 +410,7 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   // stream words <= SUB_max x code words + 2 pad words
   if ((s = ctx->grow(&ctx->codestream.p, &ctx->codestream.cap, ((size_t)4 * (n_nodes + n) + 2) * sizeof(uint4), "stream"))) return s;
   if ((s = ctx->grow(&ctx->status.p, &ctx->status.cap, (size_t)n * sizeof(uint32_t), "status"))) return s;
+  if ((s = ctx->grow(&ctx->inv.p, &ctx->inv.cap, (size_t)(n + kNumVariants + 1) * sizeof(int32_t), "inv"))) return s;
   if ((s = ctx->grow(&ctx->scratch.p, &ctx->scratch.cap, (size_t)4 * n_nodes * sizeof(int32_t), "scratch"))) return s;
   if ((s = ctx->launch(launch_stage(programs, offsets, n_programs, n_nodes, n_cols, max_stack,
                                   (uint4*)ctx->code.p, (int64_t*)ctx->code_off.p,
@@ -391,7 +418,6 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
                                   (uint32_t*)ctx->status.p, (int32_t*)ctx->scratch.p,
                                   ctx->sethi_ullman ? 1 : 0, ctx->stream),
                      "stage kernel"))) return s;
-  const float* shift = nullptr;
   if (pearson) {  // DESIGN.md C9: K_p = f_p(reference row), K_y = y_ref
     if ((s = ctx->grow(&ctx->shift.p, &ctx->shift.cap, (size_t)n * sizeof(float) + 16, "shift"))) return s;
     float* sh = (float*)ctx->shift.p;
@@ -401,6 +427,19 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
       xref = (const float*)ctx->xref.p;
       stride = 1;
       yref = (const float*)ctx->xref.p + ctx->xref_cols;
+    } else if (ctx->comm && ctx->shard == GP_SHARD_ROWS) {
+      // no reference row set and rows are sharded: every rank must shift by the SAME row, so
+      // rank 0's first row (and y) is broadcast (local rows would mix shifts)
+      if ((s = ctx->grow(&ctx->xref_b.p, &ctx->xref_b.cap, (size_t)(n_cols + 1) * sizeof(float), "xref_b"))) return s;
+      float* xb = (float*)ctx->xref_b.p;
+      if ((s = ctx->launch(launch_gather_row(X, ldx, n_cols, y, xb, ctx->stream), "gather row"))) return s;
+      NcclApi& nc = nccl();
+      ncclResult_t r = nc.Broadcast(xb, xb, (size_t)n_cols + 1, ncclFloat32, 0,
+                                    (ncclComm_t)ctx->comm, ctx->stream);
+      if (r != ncclSuccess) return ctx->fail(GP_ERR_NCCL, "ncclBroadcast: %s", nc.GetErrorString(r));
+      xref = xb;
+      stride = 1;
+      yref = xb + n_cols;
     } else {
       xref = X;
       stride = ldx;
@@ -410,7 +449,6 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
     if ((s = ctx->launch(launch_shift((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
                                     (const int32_t*)ctx->code_len.p, n_programs, kCaseStride,
                                     xref, stride, sh, ctx->stream), "shift kernel"))) return s;
-    shift = sh;
   }
   return bucket_pack(ctx, n_programs, G, skip_const, p_lo, p_hi < 0 ? n_programs : p_hi);
 }
@@ -427,7 +465,7 @@ static gp_status bucket_pack(gp_context* ctx, int32_t n_programs, int32_t G, boo
   if ((s = ctx->launch(launch_bucket((const int32_t*)ctx->need.p, (const int32_t*)ctx->code_len.p,
                                    n_programs, G, subs, (int32_t*)ctx->lists.p, (int64_t*)ctx->pos.p,
                                    (int64_t*)ctx->gstart.p, counts, base, skip_const ? 1 : 0,
-                                   p_lo, p_hi, ctx->stream),
+                                   p_lo, p_hi, (int32_t*)ctx->inv.p, ctx->stream),
                      "bucket kernel"))) return s;
   return ctx->launch(launch_pack((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
                                (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->lists.p,
@@ -482,7 +520,8 @@ static gp_status evaluate_spearman(gp_context* ctx, const gp_node* programs,
   const int32_t chunk = by_prog ? (n_programs + ctx->world - 1) / ctx->world : n_programs;
   const int32_t p_lo = by_prog ? std::min(n_programs, ctx->rank * chunk) : 0;
   const int32_t p_hi = by_prog ? std::min(n_programs, p_lo + chunk) : n_programs;
-  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, 1, true, false);
+  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, 1, true, false,
+                                ctx->plan_G, ctx->plan_tpc);
   // compile every program (no bucket work yet: empty range)
   if ((s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, n_rows,
                    n_cols, pl.G, false, nullptr, &any_host, false, 0, 0))) return s;
@@ -546,6 +585,97 @@ static gp_status evaluate_spearman(gp_context* ctx, const gp_node* programs,
   return GP_OK;
 }
 
+// The per-rank half of an evaluation: compile, dataset constants, fused evaluator
+// launches, fixed-order reduction over row chunks -> ctx->sums (compact layout, kernels.h
+// kConstCols). Shared by gp_evaluate and gp_evaluate_partial.
+struct EvalRun {
+  EvalPlan pl;
+  int S = 1;
+  bool closed = false, by_prog = false;
+  int32_t chunk = 0, p_lo = 0, p_hi = 0;
+  int64_t ld_part = 0;
+};
+
+static gp_status eval_sums(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
+                           int32_t n_programs, int64_t n_nodes, int32_t max_stack, const float* X,
+                           int64_t ldx, const float* y, const float* w, int64_t n_rows,
+                           int32_t n_cols, gp_metric metric, bool* any_host, EvalRun* run) {
+  gp_status s;
+  const int S = metric == GP_PEARSON ? 3 : 1;
+  run->S = S;
+  run->pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, S, false, w != nullptr,
+                      ctx->plan_G, ctx->plan_tpc);
+  const EvalPlan& pl = run->pl;
+  // variable-free programs: closed form in finalize for MSE / RMSE / LogLoss / Pearson (not MAE)
+  run->closed = ctx->const_programs && metric != GP_MAE;
+  // population sharding (SURVEY F3): every rank holds all rows and evaluates the programs
+  // [lo, hi) of equal-count chunks; fitness / status are all-gathered after finalize.
+  // Without a communicator gp_context_set_program_range selects the range.
+  run->by_prog = ctx->comm && ctx->shard == GP_SHARD_PROGRAMS;
+  run->chunk = run->by_prog ? (n_programs + ctx->world - 1) / ctx->world : n_programs;
+  if (run->by_prog) {
+    run->p_lo = std::min(n_programs, ctx->rank * run->chunk);
+    run->p_hi = std::min(n_programs, run->p_lo + run->chunk);
+  } else {
+    run->p_lo = std::min(n_programs, ctx->range_lo);
+    run->p_hi = ctx->range_hi < 0 ? n_programs : std::min(n_programs, ctx->range_hi);
+  }
+  if ((s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, n_rows,
+                   n_cols, pl.G, metric == GP_PEARSON, y, any_host, run->closed, run->p_lo,
+                   run->p_hi))) return s;
+
+  // Fused evaluation -> partial sums (compact columns: constants, then evaluated programs)
+  const int64_t ld_part = kConstCols + (int64_t)n_programs * S;
+  run->ld_part = ld_part;
+  if ((s = ctx->grow(&ctx->partial.p, &ctx->partial.cap, (size_t)pl.n_chunks * ld_part * sizeof(double), "partial"))) return s;
+  if ((s = ctx->grow(&ctx->sums.p, &ctx->sums.cap, (size_t)ld_part * sizeof(double), "sums"))) return s;
+  EvalArgs a{};
+  a.X = X;
+  a.ldx = ldx;
+  a.y = y;
+  a.w = w;
+  a.n_rows = n_rows;
+  a.n_cols = n_cols;
+  a.n_programs = n_programs;
+  a.metric = metric;
+  a.G = pl.G;
+  a.rows_per_chunk = pl.rows_per_chunk;
+  a.n_chunks = pl.n_chunks;
+  a.partial = (double*)ctx->partial.p;
+  a.ld_part = ld_part;
+  a.shift = metric == GP_PEARSON ? (const float*)ctx->shift.p : nullptr;
+  a.y_shift = metric == GP_PEARSON ? (const float*)ctx->shift.p + n_programs : nullptr;
+  ctx->last_plan = pl;
+  if ((s = ctx->launch(launch_consts(y, w, n_rows, pl.rows_per_chunk, pl.n_chunks, a.y_shift,
+                                   a.partial, ld_part, 0, metric == GP_LOGLOSS ? 1 : 0,
+                                   ctx->stream),
+                     "consts kernel"))) return s;
+  if ((s = launch_variants(ctx, a, pl, max_stack, false))) return s;
+  return ctx->launch(launch_tile_reduce((const double*)ctx->partial.p, pl.n_chunks, ld_part,
+                                        (const int32_t*)ctx->inv.p + n_programs + kNumVariants, S,
+                                        (double*)ctx->sums.p, ctx->stream),
+                     "tile_reduce");
+}
+
+// Fitness / status to the caller's buffers after finalize (+ the program-shard all-gather).
+static gp_status deliver(gp_context* ctx, const EvalRun& run, int32_t n_programs, float* fit_dev,
+                         float* fitness_out, uint32_t* status_out, bool fit_host, bool st_host,
+                         bool any_host) {
+  gp_status s;
+  if (run.by_prog && (s = gather_programs(ctx, n_programs, run.chunk, run.p_lo, run.p_hi, fit_dev))) return s;
+  if (fit_host) {
+    if ((s = ctx->cuda(cudaMemcpyAsync(fitness_out, fit_dev, (size_t)n_programs * sizeof(float),
+                                       cudaMemcpyDeviceToHost, ctx->stream), "D2H fitness"))) return s;
+  }
+  if (status_out) {
+    if ((s = ctx->cuda(cudaMemcpyAsync(status_out, ctx->status.p, (size_t)n_programs * sizeof(uint32_t),
+                                       st_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                       ctx->stream), "status copy"))) return s;
+  }
+  if (any_host || fit_host || st_host) return ctx->cuda(cudaStreamSynchronize(ctx->stream), "sync");
+  return GP_OK;
+}
+
 gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
                       int32_t n_programs, int64_t n_nodes, int32_t max_stack, const float* X,
                       int64_t ldx, const float* y, const float* w, int64_t n_rows, int32_t n_cols,
@@ -569,52 +699,15 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
     return evaluate_spearman(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, y,
                              w, n_rows, n_cols, fitness_out, status_out, fit_host, st_host,
                              any_host);
-  const int S = metric == GP_PEARSON ? 3 : 1;
-  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, S, false, w != nullptr);
-  // variable-free programs: closed form in finalize for MSE / RMSE / LogLoss / Pearson (not MAE)
-  const bool closed = ctx->const_programs && metric != GP_MAE;
-  // population sharding (SURVEY F3): every rank holds all rows and evaluates the programs
-  // [lo, hi) of equal-count chunks; fitness / status are all-gathered after finalize
-  const bool by_prog = ctx->comm && ctx->shard == GP_SHARD_PROGRAMS;
-  const int32_t chunk = by_prog ? (n_programs + ctx->world - 1) / ctx->world : n_programs;
-  const int32_t p_lo = by_prog ? std::min(n_programs, ctx->rank * chunk) : 0;
-  const int32_t p_hi = by_prog ? std::min(n_programs, p_lo + chunk) : n_programs;
-  if ((s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, n_rows,
-                   n_cols, pl.G, metric == GP_PEARSON, y, &any_host, closed, p_lo, p_hi))) return s;
-
-  // Fused evaluation -> partial sums
-  const int64_t ld_part = (int64_t)n_programs * S + 3;
-  if ((s = ctx->grow(&ctx->partial.p, &ctx->partial.cap, (size_t)pl.n_chunks * ld_part * sizeof(double), "partial"))) return s;
-  if ((s = ctx->grow(&ctx->sums.p, &ctx->sums.cap, (size_t)ld_part * sizeof(double), "sums"))) return s;
-  EvalArgs a{};
-  a.X = X;
-  a.ldx = ldx;
-  a.y = y;
-  a.w = w;
-  a.n_rows = n_rows;
-  a.n_cols = n_cols;
-  a.n_programs = n_programs;
-  a.metric = metric;
-  a.G = pl.G;
-  a.rows_per_chunk = pl.rows_per_chunk;
-  a.n_chunks = pl.n_chunks;
-  a.partial = (double*)ctx->partial.p;
-  a.ld_part = ld_part;
-  a.shift = metric == GP_PEARSON ? (const float*)ctx->shift.p : nullptr;
-  a.y_shift = metric == GP_PEARSON ? (const float*)ctx->shift.p + n_programs : nullptr;
-  ctx->last_plan = pl;
-  if ((s = ctx->launch(launch_consts(y, w, n_rows, pl.rows_per_chunk, pl.n_chunks, a.y_shift,
-                                   a.partial, ld_part, (int64_t)n_programs * S,
-                                   metric == GP_LOGLOSS ? 1 : 0, ctx->stream),
-                     "consts kernel"))) return s;
-  if ((s = launch_variants(ctx, a, pl, max_stack, false))) return s;
-  if ((s = ctx->launch(launch_tile_reduce((const double*)ctx->partial.p, pl.n_chunks, ld_part,
-                                        (double*)ctx->sums.p, ctx->stream), "tile_reduce"))) return s;
-  // A6: one all-reduce of the fp64 partial sums across ranks (rows are sharded)
-  if (ctx->comm && !by_prog) {
+  EvalRun run;
+  if ((s = eval_sums(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, y, w,
+                     n_rows, n_cols, metric, &any_host, &run))) return s;
+  // A6: one all-reduce of the fp64 sums across ranks (rows are sharded; every rank has the same
+  // compact layout because it holds the same population)
+  if (ctx->comm && !run.by_prog) {
     NcclApi& n = nccl();
-    ncclResult_t r = n.AllReduce(ctx->sums.p, ctx->sums.p, (size_t)ld_part, ncclFloat64, ncclSum,
-                                 (ncclComm_t)ctx->comm, ctx->stream);
+    ncclResult_t r = n.AllReduce(ctx->sums.p, ctx->sums.p, (size_t)run.ld_part, ncclFloat64,
+                                 ncclSum, (ncclComm_t)ctx->comm, ctx->stream);
     if (r != ncclSuccess) return ctx->fail(GP_ERR_NCCL, "ncclAllReduce: %s", n.GetErrorString(r));
   }
   // A7: finalize
@@ -623,23 +716,94 @@ gp_status gp_evaluate(gp_context* ctx, const gp_node* programs, const int64_t* n
     if ((s = ctx->grow(&ctx->h_fit.p, &ctx->h_fit.cap, (size_t)n_programs * sizeof(float), "fit"))) return s;
     fit_dev = (float*)ctx->h_fit.p;
   }
-  if ((s = ctx->launch(launch_finalize((const double*)ctx->sums.p, n_programs, metric,
-                                     (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->need.p,
-                                     (const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
-                                     closed ? 1 : 0, fit_dev,
-                                     (uint32_t*)ctx->status.p, ctx->stream), "finalize"))) return s;
-  if (by_prog && (s = gather_programs(ctx, n_programs, chunk, p_lo, p_hi, fit_dev))) return s;
-  if (fit_host) {
-    if ((s = ctx->cuda(cudaMemcpyAsync(fitness_out, fit_dev, (size_t)n_programs * sizeof(float),
-                                       cudaMemcpyDeviceToHost, ctx->stream), "D2H fitness"))) return s;
+  const double* sums = (const double*)ctx->sums.p;
+  if ((s = ctx->launch(launch_finalize(sums, sums + kConstCols, (const int32_t*)ctx->inv.p,
+                                       n_programs, metric,
+                                       (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->need.p,
+                                       (const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
+                                       run.closed ? 1 : 0, fit_dev,
+                                       (uint32_t*)ctx->status.p, ctx->stream), "finalize"))) return s;
+  return deliver(ctx, run, n_programs, fit_dev, fitness_out, status_out, fit_host, st_host, any_host);
+}
+
+gp_status gp_evaluate_partial(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
+                              int32_t n_programs, int64_t n_nodes, int32_t max_stack,
+                              const float* X, int64_t ldx, const float* y, const float* w,
+                              int64_t n_rows, int32_t n_cols, gp_metric metric, double* sums_out) {
+  if (!ctx) return GP_ERR_ARG;
+  cudaSetDevice(ctx->device);
+  if ((int)metric < 0 || (int)metric > GP_SPEARMAN || !y || !sums_out)
+    return ctx->fail(GP_ERR_ARG, "invalid metric / y / sums_out");
+  if (metric == GP_SPEARMAN)
+    return ctx->fail(GP_ERR_UNSUPPORTED, "Spearman ranks are not additive over row shards");
+  if (ctx->comm && ctx->shard == GP_SHARD_PROGRAMS)
+    return ctx->fail(GP_ERR_ARG, "gp_evaluate_partial: program sharding has no row partials");
+  bool any_host = false;
+  gp_status s;
+  const void* d;
+  if ((s = ctx->stage_in(y, (size_t)n_rows * sizeof(float), ctx->h_y, &d, &any_host))) return s;
+  y = (const float*)d;
+  if (w) {
+    if ((s = ctx->stage_in(w, (size_t)n_rows * sizeof(float), ctx->h_w, &d, &any_host))) return s;
+    w = (const float*)d;
   }
-  if (status_out) {
-    if ((s = ctx->cuda(cudaMemcpyAsync(status_out, ctx->status.p, (size_t)n_programs * sizeof(uint32_t),
-                                       st_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
-                                       ctx->stream), "status copy"))) return s;
+  EvalRun run;
+  if ((s = eval_sums(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx, y, w,
+                     n_rows, n_cols, metric, &any_host, &run))) return s;
+  const bool out_host = is_host_pointer(sums_out);
+  double* dst = sums_out;
+  const size_t bytes = (size_t)run.ld_part * sizeof(double);
+  if (out_host) {
+    if ((s = ctx->grow(&ctx->sums_x.p, &ctx->sums_x.cap, bytes, "sums_x"))) return s;
+    dst = (double*)ctx->sums_x.p;
   }
-  if (any_host || fit_host || st_host) return ctx->cuda(cudaStreamSynchronize(ctx->stream), "sync");
+  if ((s = ctx->launch(launch_expand_sums((const double*)ctx->sums.p, (const int32_t*)ctx->inv.p,
+                                          n_programs, run.S, dst, ctx->stream), "expand sums"))) return s;
+  if (out_host) {
+    if ((s = ctx->cuda(cudaMemcpyAsync(sums_out, dst, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H sums"))) return s;
+  }
+  if (any_host || out_host) return ctx->cuda(cudaStreamSynchronize(ctx->stream), "sync");
   return GP_OK;
+}
+
+gp_status gp_finalize_sums(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
+                           int32_t n_programs, int64_t n_nodes, int32_t max_stack, int32_t n_cols,
+                           const double* sums, gp_metric metric, float* fitness_out,
+                           uint32_t* status_out) {
+  if (!ctx) return GP_ERR_ARG;
+  cudaSetDevice(ctx->device);
+  if ((int)metric < 0 || (int)metric >= GP_SPEARMAN || !sums || !fitness_out)
+    return ctx->fail(GP_ERR_ARG, "invalid metric / sums / fitness_out");
+  bool any_host = false;
+  gp_status s;
+  const int S = metric == GP_PEARSON ? 3 : 1;
+  const void* d;
+  if ((s = ctx->stage_in(sums, ((size_t)n_programs * S + kConstCols) * sizeof(double), ctx->sums_x, &d, &any_host))) return s;
+  const double* sd = (const double*)d;
+  // compile (status bits, closed-form constants); a dummy 1-row X is never read by the stage
+  // kernel, so only the column count matters
+  EvalRun run;
+  run.S = S;
+  run.closed = ctx->const_programs && metric != GP_MAE;
+  run.p_lo = 0;
+  run.p_hi = n_programs;
+  const float* Xdummy = (const float*)sd;
+  if ((s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, Xdummy, 1, 1,
+                   n_cols, 1, false, nullptr, &any_host, run.closed, 0, 0))) return s;
+  const bool fit_host = is_host_pointer(fitness_out);
+  const bool st_host = status_out && is_host_pointer(status_out);
+  float* fit_dev = fitness_out;
+  if (fit_host) {
+    if ((s = ctx->grow(&ctx->h_fit.p, &ctx->h_fit.cap, (size_t)n_programs * sizeof(float), "fit"))) return s;
+    fit_dev = (float*)ctx->h_fit.p;
+  }
+  if ((s = ctx->launch(launch_finalize(sd + (int64_t)n_programs * S, sd, nullptr, n_programs,
+                                       metric, (const int32_t*)ctx->code_len.p,
+                                       (const int32_t*)ctx->need.p, (const uint4*)ctx->code.p,
+                                       (const int64_t*)ctx->code_off.p, run.closed ? 1 : 0,
+                                       fit_dev, (uint32_t*)ctx->status.p, ctx->stream),
+                       "finalize"))) return s;
+  return deliver(ctx, run, n_programs, fit_dev, fitness_out, status_out, fit_host, st_host, any_host);
 }
 
 gp_status gp_predict(gp_context* ctx, const gp_node* programs, const int64_t* node_offsets,
@@ -650,7 +814,8 @@ gp_status gp_predict(gp_context* ctx, const gp_node* programs, const int64_t* no
   cudaSetDevice(ctx->device);
   if (!out || ld_out < n_rows) return ctx->fail(GP_ERR_ARG, "invalid out / ld_out");
   bool any_host = false;
-  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, 1, true, false);
+  const EvalPlan pl = plan_eval(ctx->device, n_rows, n_programs, n_cols, 1, true, false,
+                                ctx->plan_G, ctx->plan_tpc);
   gp_status s = prepare(ctx, programs, node_offsets, n_programs, n_nodes, max_stack, X, ldx,
                         n_rows, n_cols, pl.G, false, nullptr, &any_host);
   if (s) return s;

@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
                                                       int32_t* __restrict__ counts,
                                                       int64_t* __restrict__ base, int4 sub4,
                                                       int32_t skip_const, int32_t p_lo,
-                                                      int32_t p_hi) {
+                                                      int32_t p_hi, int32_t* __restrict__ inv) {
   __shared__ int warp_cnt[kNumVariants][32];
   __shared__ int cnt[kNumVariants];
   __shared__ int64_t warp_tot[32];
@@ -302,15 +302,27 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
   }
   if (tid == 0) base[kNumVariants] = running;
   if (tid < kNumVariants) counts[tid] = cnt[tid];
+  // phase 3: compact partial-sum positions (kernels.h kConstCols): bucket b's programs follow
+  // those of buckets < b; inv[p] = position or -1 (not evaluated); inv[n + b] = first position of
+  // bucket b, inv[n + kNumVariants] = evaluated programs in total
+  for (int p = tid; p < n; p += 1024) inv[p] = -1;
+  __syncthreads();
+  int pb = 0;
+  for (int b = 0; b < kNumVariants; ++b) {
+    if (tid == 0) inv[n + b] = pb;
+    for (int j = tid; j < cnt[b]; j += 1024) inv[lists[(int64_t)b * n + j]] = pb + j;
+    pb += cnt[b];
+  }
+  if (tid == 0) inv[n + kNumVariants] = pb;
 }
 
 cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
                           int32_t G, const int* subs, int32_t* lists, int64_t* pos,
                           int64_t* gstart, int32_t* counts, int64_t* base, int32_t skip_const,
-                          int32_t p_lo, int32_t p_hi, cudaStream_t s) {
+                          int32_t p_lo, int32_t p_hi, int32_t* inv, cudaStream_t s) {
   bucket_kernel<<<1, 1024, 0, s>>>(need, code_len, n_programs, G, lists, pos, gstart, counts,
                                    base, make_int4(subs[0], subs[1], subs[2], subs[3]), skip_const,
-                                   p_lo, p_hi);
+                                   p_lo, p_hi, inv);
   return cudaGetLastError();
 }
 
@@ -460,23 +472,85 @@ cudaError_t launch_copy_scalar(const float* src, float* dst, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Cross-work-item reduction: sums[j] = sum_{q < n_chunks} partial[q][j], in fixed q
-// order -> run-to-run deterministic.
+// Cross-work-item reduction: sums[j] = sum over the n_chunks row chunks of
+// partial[q][j] for the live columns j < kConstCols + S * (evaluated programs) (count read on the
+// device: inv[n + kNumVariants]). CTA = 32 columns x 8 chunk slices: thread (x, y) sums the
+// chunks of slice y in ascending q, the 8 slice sums are then added in ascending y. The order is
+// fixed for a given n_chunks -> run-to-run deterministic; 32 consecutive columns per warp
+// -> 256-byte coalesced rows; 8 independent load streams per column.
 // ---------------------------------------------------------------------------------------------
-__global__ void tile_reduce_kernel(const double* __restrict__ partial, int64_t n_chunks,
-                                   int64_t ld, double* __restrict__ sums) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= ld) return;
-  double s = 0.0;
-  for (int64_t q = 0; q < n_chunks; ++q) s += partial[q * ld + j];
-  sums[j] = s;
+constexpr int kTrCols = 32, kTrSlices = 8;
+__global__ void __launch_bounds__(kTrCols * kTrSlices)
+    tile_reduce_kernel(const double* __restrict__ partial, int64_t n_chunks, int64_t ld,
+                       const int32_t* __restrict__ live, int32_t S, double* __restrict__ sums) {
+  __shared__ double part[kTrSlices][kTrCols];
+  const int64_t n_live = kConstCols + (int64_t)S * (*live);
+  const int64_t j = (int64_t)blockIdx.x * kTrCols + threadIdx.x;
+  if ((int64_t)blockIdx.x * kTrCols >= n_live) return;      // whole CTA past the live columns
+  const int y = threadIdx.y;
+  const int64_t per = (n_chunks + kTrSlices - 1) / kTrSlices;
+  const int64_t q0 = y * per, q1 = min(n_chunks, q0 + per);
+  double a0 = 0.0, a1 = 0.0;                                   // even / odd chunks of the slice
+  if (j < n_live) {
+    int64_t q = q0;
+    for (; q + 1 < q1; q += 2) {
+      a0 += partial[q * ld + j];
+      a1 += partial[(q + 1) * ld + j];
+    }
+    if (q < q1) a0 += partial[q * ld + j];
+  }
+  part[y][threadIdx.x] = a0 + a1;
+  __syncthreads();
+  if (y == 0 && j < n_live) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < kTrSlices; ++k) t += part[k][threadIdx.x];
+    sums[j] = t;
+  }
 }
 
 cudaError_t launch_tile_reduce(const double* partial, int64_t n_chunks, int64_t ld_part,
-                               double* sums, cudaStream_t s) {
-  const int nt = 256;
-  tile_reduce_kernel<<<(unsigned)((ld_part + nt - 1) / nt), nt, 0, s>>>(partial, n_chunks,
-                                                                          ld_part, sums);
+                               const int32_t* live, int32_t S, double* sums, cudaStream_t s) {
+  const dim3 blk(kTrCols, kTrSlices);
+  tile_reduce_kernel<<<(unsigned)((ld_part + kTrCols - 1) / kTrCols), blk, 0, s>>>(
+      partial, n_chunks, ld_part, live, S, sums);
+  return cudaGetLastError();
+}
+
+// Compact (bucket-order) sums -> program order: out[p S + k] = sums of p or 0 if p was not
+// evaluated per row; out[n S + c] = dataset constant c. (gp_evaluate_partial's output layout.)
+__global__ void expand_sums_kernel(const double* __restrict__ sums, const int32_t* __restrict__ inv,
+                                   int32_t n, int32_t S, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nS = (int64_t)n * S;
+  if (i < nS) {
+    const int p = (int)(i / S), k = (int)(i - (int64_t)p * S);
+    const int c = inv[p];
+    out[i] = c >= 0 ? sums[kConstCols + (int64_t)c * S + k] : 0.0;
+  } else if (i < nS + kConstCols) {
+    out[i] = sums[i - nS];
+  }
+}
+
+cudaError_t launch_expand_sums(const double* sums, const int32_t* inv, int32_t n, int32_t S,
+                               double* out, cudaStream_t s) {
+  const int64_t total = (int64_t)n * S + kConstCols;
+  expand_sums_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(sums, inv, n, S, out);
+  return cudaGetLastError();
+}
+
+// Row 0 of this rank's shard (X[c * ldx], y[0]) -> dst[0..n_cols] (the Pearson reference row that
+// rank 0 broadcasts when the caller did not set one).
+__global__ void gather_row_kernel(const float* __restrict__ X, int64_t ldx, int32_t n_cols,
+                                  const float* __restrict__ y, float* __restrict__ dst) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n_cols) dst[c] = X[(int64_t)c * ldx];
+  if (c == n_cols) dst[c] = y[0];
+}
+
+cudaError_t launch_gather_row(const float* X, int64_t ldx, int32_t n_cols, const float* y,
+                              float* dst, cudaStream_t s) {
+  gather_row_kernel<<<(n_cols + 1 + 127) / 128, 128, 0, s>>>(X, ldx, n_cols, y, dst);
   return cudaGetLastError();
 }
 
@@ -484,7 +558,8 @@ cudaError_t launch_tile_reduce(const double* partial, int64_t n_chunks, int64_t 
 // Finalize: per-program sums (+ dataset constants W, S_y, S_yy at the end) ->
 // raw fitness ("vector containing final raw fitness values"), S:201 normalisation.
 // ---------------------------------------------------------------------------------------------
-__global__ void finalize_kernel(const double* __restrict__ sums, int32_t n_programs,
+__global__ void finalize_kernel(const double* __restrict__ consts, const double* __restrict__ psums,
+                                const int32_t* __restrict__ idx, int32_t n_programs,
                                 int32_t metric, const int32_t* __restrict__ code_len,
                                 const int32_t* __restrict__ need, const uint4* __restrict__ code,
                                 const int64_t* __restrict__ code_off, int32_t closed_const,
@@ -492,8 +567,12 @@ __global__ void finalize_kernel(const double* __restrict__ sums, int32_t n_progr
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_programs) return;
   const int S = metric == GP_PEARSON ? 3 : 1;
-  const int64_t nS = (int64_t)n_programs * S;
-  const double W = sums[nS], Sy = sums[nS + 1], Syy = sums[nS + 2];
+  const double W = consts[0], Sy = consts[1], Syy = consts[2];
+  // this program's S sums: compact position idx[p] (-1: not evaluated per row -> zeros), or
+  // program order when idx is null
+  const int64_t pos = idx ? (int64_t)idx[p] : (int64_t)p;
+  const double zero3[3] = {0.0, 0.0, 0.0};
+  const double* sums = pos >= 0 ? psums + pos * S : zero3;
   uint32_t fl = status[p];
   float out;
   // closed_const: variable-free programs (need 0) were not evaluated per row; their sums follow
@@ -520,14 +599,13 @@ __global__ void finalize_kernel(const double* __restrict__ sums, int32_t n_progr
       f = (W * c * c - 2.0 * c * Sy + Syy) / W;
       if (f < 0.0) f = 0.0;                        // rounding; NaN / inf pass through
     } else {
-      f = sums[p] / W;
+      f = sums[0] / W;
     }
     if (metric == GP_RMSE) f = sqrt(f);
     if (!isfinite(f) || f > (double)FLT_MAX) { f = INFINITY; fl |= GP_FLAG_NONFINITE; }
     out = (float)f;
   } else {
-    const double Sd = cst ? 0.0 : sums[3 * (int64_t)p], Sdd = cst ? 0.0 : sums[3 * (int64_t)p + 1],
-                 Sdy = cst ? 0.0 : sums[3 * (int64_t)p + 2];
+    const double Sd = cst ? 0.0 : sums[0], Sdd = cst ? 0.0 : sums[1], Sdy = cst ? 0.0 : sums[2];
     const double cov = Sdy - Sd * Sy / W, vd = Sdd - Sd * Sd / W, vy = Syy - Sy * Sy / W;
     double r = cov / sqrt(vd * vy);
     if (!(vd > 0.0) || !(vy > 0.0) || !isfinite(r)) { r = 0.0; fl |= GP_FLAG_UNDEFINED_CORR; }
@@ -538,12 +616,13 @@ __global__ void finalize_kernel(const double* __restrict__ sums, int32_t n_progr
   status[p] = fl;
 }
 
-cudaError_t launch_finalize(const double* sums, int32_t n_programs, int32_t metric,
+cudaError_t launch_finalize(const double* consts, const double* psums, const int32_t* idx,
+                            int32_t n_programs, int32_t metric,
                             const int32_t* code_len, const int32_t* need, const uint4* code,
                             const int64_t* code_off, int32_t closed_const, float* fitness,
                             uint32_t* status, cudaStream_t s) {
   const int nt = 128;
-  finalize_kernel<<<(n_programs + nt - 1) / nt, nt, 0, s>>>(sums, n_programs, metric, code_len,
+  finalize_kernel<<<(n_programs + nt - 1) / nt, nt, 0, s>>>(consts, psums, idx, n_programs, metric, code_len,
                                                              need, code, code_off, closed_const,
                                                              fitness, status);
   return cudaGetLastError();

@@ -15,11 +15,14 @@ cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n
 // Partitions valid programs by stack need into kNumVariants ascending lists, lays out each
 // variant's code stream (per-program offsets, group starts for G programs per group), zeroes the
 // work counters. lists/pos: [kNumVariants][n_programs]; gstart: [kNumVariants][n_programs + 1];
-// counts: [kNumVariants] then counters [kNumVariants]; base: [kNumVariants + 1] stream bases.
+// counts: [kNumVariants] then counters [kNumVariants]; base: [kNumVariants + 1] stream bases;
+// inv: [n] compact partial-sum position of each program (-1: not evaluated), then
+// [kNumVariants + 1] bucket start positions and the evaluated total.
 cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
                           int32_t G, const int* subs, int32_t* lists, int64_t* pos,
                           int64_t* gstart, int32_t* counts, int64_t* base, int32_t skip_const,
-                          int32_t p_lo, int32_t p_hi, cudaStream_t s);
+                          int32_t p_lo, int32_t p_hi, int32_t* inv /* n + kNumVariants + 1 */,
+                          cudaStream_t s);
 // Copies every bucketed program's code into its variant stream, flagging the end of each pass
 // and of each shared-memory stream window (kernels.h kEndWin).
 cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
@@ -33,11 +36,20 @@ cudaError_t launch_consts(const float* y, const float* w, int64_t n_rows, int64_
 cudaError_t launch_shift(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                          int32_t n_programs, int32_t stack_cap, const float* xref,
                          int64_t xref_stride, float* shift_out, cudaStream_t s);
+// sums[j] = fixed-order sum over row chunks of partial[q][j], j < kConstCols + S * (*live)
 cudaError_t launch_tile_reduce(const double* partial, int64_t n_chunks, int64_t ld_part,
-                               double* sums, cudaStream_t s);
+                               const int32_t* live, int32_t S, double* sums, cudaStream_t s);
+// compact sums -> program order [n][S] (0 for programs not evaluated) + the kConstCols constants
+cudaError_t launch_expand_sums(const double* sums, const int32_t* inv, int32_t n, int32_t S,
+                               double* out, cudaStream_t s);
+// dst[0 .. n_cols) = row 0 of X, dst[n_cols] = y[0]
+cudaError_t launch_gather_row(const float* X, int64_t ldx, int32_t n_cols, const float* y,
+                              float* dst, cudaStream_t s);
 // closed_const: variable-free programs (need 0) skipped by the evaluator get their loss from the
 // dataset moments (MSE / RMSE) or an undefined correlation (Pearson).
-cudaError_t launch_finalize(const double* sums, int32_t n_programs, int32_t metric,
+// consts: W, S_y, S_yy; psums: S sums per program at position idx[p] (null: p; -1: none)
+cudaError_t launch_finalize(const double* consts, const double* psums, const int32_t* idx,
+                            int32_t n_programs, int32_t metric,
                             const int32_t* code_len, const int32_t* need, const uint4* code,
                             const int64_t* code_off, int32_t closed_const, float* fitness,
                             uint32_t* status, cudaStream_t s);

@@ -522,7 +522,9 @@ gp_status gp_engine_create(gp_engine** out, gp_context* ctx, const gp_config* cf
   e->ctx = ctx;
   e->cfg = c;
   e->higher = c.metric == GP_PEARSON || c.metric == GP_SPEARMAN;  // correlations: higher wins
-  e->threads = c.n_threads > 0 ? c.n_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  // default: this rank's share of the host cores (every rank of a node runs the same host steps)
+  e->threads = c.n_threads > 0 ? c.n_threads
+                               : std::max(1, (int)std::thread::hardware_concurrency() / std::max(1, ctx->world));
   // one generation's host work is O(population); beyond 64 threads wake-ups cost more than they save
   e->pool.reset(new Pool(std::min(e->threads, 64)));
   gp_status s = e->set_dataset(X, ldx, y, w, n_rows, n_cols);

@@ -20,8 +20,8 @@
 //         run time (the paper's unrolled slot loop, costs O(capacity) per push) [A3]
 //       fused weighted loss of those rows (no m x n prediction matrix)             [A4]
 //       warp shuffle reduction, lane 0 accumulates into a per-(warp, program) fp64 smem slot   [A5]
-//   per-program sums over warps in fixed order -> partial[q][p] (no atomics on data: the sums do
-//   not depend on which CTA ran which item)
+//   per-program sums over warps in fixed order -> partial[q][bucket position] (no atomics on data:
+//   the sums do not depend on which CTA ran which item)
 //
 // The paper's design is one thread per row and a (ceil(m/256), n) grid; here each thread
 // owns R*SUB rows and loops over programs, so X is read from HBM about once (program groups are
@@ -439,12 +439,16 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
 
     if constexpr (!PREDICT) {
       __syncthreads();
-      double* prow = a.partial + q * a.ld_part;
+      // compact layout: the program in bucket slot j of this variant owns partial column
+      // kConstCols + (part_base + j) * S (part_base = programs of the lower-capacity buckets), so
+      // only programs that were evaluated per row are written and tile-reduced
+      double* prow = a.partial + q * a.ld_part + kConstCols +
+                     ((int64_t)*a.part_base + (int64_t)g * a.G) * S;
       for (int j = tid; j < np * S; j += NT) {
         const int pl = j / S, k = j - pl * S;
         double sum = 0.0;
         for (int wv = 0; wv < NW; ++wv) sum += acc[((size_t)wv * a.G + pl) * S + k];
-        prow[(int64_t)gids[pl] * S + k] = sum;
+        prow[j] = sum;
       }
     }
   }

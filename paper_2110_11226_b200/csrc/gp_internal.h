@@ -25,7 +25,7 @@ struct EvalPlan {
 bool is_host_pointer(const void* p);
 int sm_count(int device);
 EvalPlan plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t n_cols, int S,
-                   bool predict, bool weighted);
+                   bool predict, bool weighted, int force_G = 0, int64_t force_tpc = 0);
 
 }  // namespace gpb
 
@@ -36,7 +36,7 @@ struct gp_context {
   std::string err;
   // device workspaces (grown on demand, stream-ordered)
   gpb::StageBuf gather, spear, code, code_off, code_len, need, lists, pos, gstart, counts, codestream, scratch, status, partial,
-      sums, shift, xref;
+      sums, shift, xref, inv, xref_b, sums_x;
   // staging for [host] arguments
   gpb::StageBuf h_nodes, h_off, h_X, h_y, h_w, h_fit;
   std::vector<float> xref_host;
@@ -51,10 +51,13 @@ struct gp_context {
   bool sethi_ullman = true;      // gp_context_set_eval_order
   bool const_programs = true;    // gp_context_set_const_programs (closed-form constant programs)
   gp_shard shard = GP_SHARD_ROWS;  // gp_context_set_shard
+  int plan_G = 0;                // gp_context_set_plan (0 = automatic)
+  int64_t plan_tpc = 0;
+  int32_t range_lo = 0, range_hi = -1;  // gp_context_set_program_range
 
   std::vector<gpb::StageBuf*> all_buffers() {
     return {&gather, &spear, &code, &code_off, &code_len, &need, &lists, &pos, &gstart, &counts, &codestream, &scratch, &status,
-            &partial, &sums, &shift, &xref,
+            &partial, &sums, &shift, &xref, &inv, &xref_b, &sums_x,
             &h_nodes, &h_off, &h_X, &h_y, &h_w, &h_fit};
   }
   gp_status fail(gp_status s, const char* fmt, ...);

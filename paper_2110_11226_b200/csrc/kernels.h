@@ -29,6 +29,10 @@ constexpr int kStreamWin = 768;
 // programs x 32 lanes of fp32 per-lane sums, rows padded to kRedStride floats so the row-part
 // LDS.128 reads of a warp hit 32 distinct banks.
 constexpr int kRedStride = 36;
+// Partial-sum rows (per row chunk): columns 0..2 hold the dataset constants (W, S_y, S_yy; consts
+// kernel), then S sums per EVALUATED program in compact bucket order (variable-free programs
+// with a closed form and programs outside the evaluated range take no column).
+constexpr int kConstCols = 3;
 
 // Everything the fused evaluator needs for one launch (see eval_impl.cuh). Each variant runs a
 // packed CODE STREAM per program group: for every program of the group, SUB copies of its code
@@ -52,8 +56,9 @@ struct EvalArgs {
   int32_t G;                  // programs per group
   int64_t rows_per_chunk;     // rows per work item (multiple of kTile)
   int64_t n_chunks;           // row chunks; work items = ceil(count / G) * n_chunks
-  double* partial;            // FIT: [n_chunks][ld_part], ld_part = n_programs * S + 3
+  double* partial;            // FIT: [n_chunks][ld_part], ld_part = kConstCols + n_programs * S
   int64_t ld_part;
+  const int32_t* part_base;   // FIT, device: first compact partial slot of this variant's bucket
   const float* shift;         // Pearson: K_p per program
   const float* y_shift;       // Pearson: device scalar K_y
   float* out;                 // PREDICT: out[p * ld_out + i]

@@ -1,0 +1,207 @@
+"""GPU parity at the PRODUCTION work decomposition, and the multi-rank data flow simulated on one GPU.
+
+Small parity tests run at sizes where the planner picks one or two programs per group and one tile
+per work item. Here the plan is forced to the shape the benchmark runs (gp_context_set_plan):
+groups of 128 programs (full 16-program reduction blocks, code streams longer than the 768-word
+shared-memory window) and 7-tile row chunks with a ragged last chunk and tile, and EVERY program is
+compared with the oracle for all five metrics, unweighted and weighted with exact zeros (SURVEY
+rows A2-A5, A7).
+
+The multi-rank tests run the product's per-rank path on row shards (gp_evaluate_partial), combine
+the fp64 sums in rank order on the host -- the all-reduce of SURVEY row A6 made explicit -- and
+finalize (gp_finalize_sums); program chunks (GP_SHARD_PROGRAMS) are simulated with
+gp_context_set_program_range. Only one GPU is reachable here, so this is the single-GPU "simulated
+P shards" row of SURVEY section 4.
+"""
+import numpy as np
+import pytest
+
+import synth
+from tests.test_gpu_parity import _dataset, check_fitness, dev
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROWS = 253 * 253          # 64,009 rows = 31 tiles of 2048 + a ragged tile of 1,521 rows
+METRICS = ["mae", "mse", "rmse", "logloss", "pearson"]
+
+
+@pytest.fixture(scope="module")
+def gp():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2110_11226_b200 as gp
+    gp.lib()
+    return gp
+
+
+@pytest.fixture()
+def pctx(gp):
+    c = gp.Context(0)
+    yield c
+    c.close()
+
+
+def _population(n_features, seed):
+    """384 programs, in this order: 64 long left-deep chains of {+, -, *, sin, cos} (well
+    conditioned; with the Sethi-Ullman order they need <= 4 slots, so the first 128-program group
+    of the 4-slot bucket carries > 1,000 code words = several 768-word shared-memory windows),
+    272 random Table-2 programs (depth 0-6) and 48 over the whole catalog."""
+    d, do = synth.deep_population(64, seed=seed, need=(8, 14), n_features=n_features)
+    a, ao = synth.random_population(272, seed=seed, depth=(0, 6), n_features=n_features,
+                                    max_stack=8, p_terminal=0.3)
+    b, bo = synth.random_population(48, seed=seed + 1, depth=(0, 6), n_features=n_features,
+                                    funcs=synth.ALL_FUNCS, max_stack=8, p_terminal=0.3)
+    nodes = np.concatenate([d, a, b])
+    off = np.concatenate([do, ao[1:] + do[-1], bo[1:] + do[-1] + ao[-1]])
+    assert (nodes[:off[128], 0] > 1).sum() > 768           # multi-window stream in group 0
+    return nodes, off
+
+
+@pytest.fixture(scope="module")
+def oracle_cache():
+    return {}
+
+
+def _case(orc, cache, metric, weighted):
+    key = (metric, weighted)
+    if key not in cache:
+        X, y = _dataset(metric, ROWS, seed=11)
+        nodes, off = _population(X.shape[0], seed=40 + len(metric))
+        w = synth.weights(X.shape[1], seed=12) if weighted else None
+        ref, sens, flags = orc.population_fitness(nodes, off, X, y, w, metric)
+        cache[key] = (X, y, w, nodes, off, ref, sens, flags)
+    return cache[key]
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+@pytest.mark.parametrize("metric", METRICS)
+def test_production_plan_every_program(gp, pctx, orc, oracle_cache, metric, weighted):
+    X, y, w, nodes, off, ref, sens, flags = _case(orc, oracle_cache, metric, weighted)
+    assert X.shape[1] % 2048 != 0
+    pctx.set_plan(128, 7)                       # 128-program groups, 7-tile chunks (5 chunks)
+    fit, st = pctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), None if w is None else dev(w),
+                            metric=metric, max_stack=8)
+    torch.cuda.synchronize()
+    check_fitness(fit.cpu().numpy(), ref, sens, flags, metric,
+                  label=f"production plan {metric} w={weighted}")
+    # the automatic plan (small groups, one-tile items) agrees to summation order
+    pctx.set_plan(0, 0)
+    fa, sa = pctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), None if w is None else dev(w),
+                           metric=metric, max_stack=8)
+    a, b = fit.cpu().numpy(), fa.cpu().numpy()
+    fin = np.isfinite(a) & np.isfinite(b)
+    assert np.array_equal(np.isfinite(a), np.isfinite(b))
+    assert torch.equal(st, sa)
+    scale = 1.0 if metric == "pearson" else np.maximum(np.abs(a[fin]), 1e-6)
+    assert np.all(np.abs(a[fin] - b[fin]) <= 1e-4 * scale)
+
+
+@pytest.mark.parametrize("metric", ["mse", "pearson", "logloss"])
+def test_production_plan_deep_buckets(gp, pctx, orc, metric):
+    """The 12- and 20-slot variants with full 128-program groups (classic evaluation order keeps
+    the deep needs): every program against the oracle."""
+    X, y = _dataset(metric, 40_000, seed=13)
+    nodes, off = synth.deep_population(400, seed=5, need=(9, 20), n_features=X.shape[0])
+    pctx.set_eval_order(False)
+    pctx.set_plan(128, 5)
+    fit, st = pctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric=metric, max_stack=20)
+    ref, sens, flags = orc.population_fitness(nodes, off, X, y, None, metric)
+    check_fitness(fit.cpu().numpy(), ref, sens, flags, metric, label=f"deep production {metric}")
+
+
+def _shard_sum(pctx, nodes, off, X, y, w, metric, P):
+    """Per-rank sums of P contiguous row shards, added in rank order (fp64)."""
+    total = None
+    m = X.shape[1]
+    for r in range(P):
+        r0, r1 = synth.shard_rows(m, r, P)
+        Xs = np.ascontiguousarray(X[:, r0:r1])
+        ws = None if w is None else dev(w[r0:r1])
+        s = pctx.evaluate_partial(dev(nodes), dev(off), dev(Xs), dev(y[r0:r1]), ws,
+                                  metric=metric, max_stack=8).cpu().numpy()
+        total = s if total is None else total + s
+    return total
+
+
+@pytest.mark.parametrize("metric", METRICS)
+def test_row_shards_simulated(gp, pctx, orc, oracle_cache, metric):
+    """P in {2, 4, 8} row shards through the product's per-rank path, summed in
+    rank order and finalized == the one-rank fitness within 1e-4 and the oracle; identical status
+    bits. Pearson shards share the GLOBAL row 0 as reference (gp_context_set_reference_row)."""
+    X, y, w, nodes, off, ref, sens, flags = _case(orc, oracle_cache, metric, True)
+    pctx.set_reference_row(X[:, 0].copy(), float(y[0]))
+    one, st1 = pctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), dev(w), metric=metric,
+                             max_stack=8)
+    one = one.cpu().numpy()
+    # P = 1 through the split path is bit-identical to gp_evaluate
+    s1 = _shard_sum(pctx, nodes, off, X, y, w, metric, 1)
+    f1, _ = pctx.finalize_sums(dev(nodes), dev(off), torch.from_numpy(s1).cuda(), X.shape[0],
+                               metric=metric, max_stack=8)
+    assert np.array_equal(f1.cpu().numpy(), one)
+    for P in (2, 4, 8):
+        tot = _shard_sum(pctx, nodes, off, X, y, w, metric, P)
+        fit, st = pctx.finalize_sums(dev(nodes), dev(off), torch.from_numpy(tot).cuda(),
+                                     X.shape[0], metric=metric, max_stack=8)
+        fit = fit.cpu().numpy()
+        assert torch.equal(st, st1)
+        fin = np.isfinite(one)
+        assert np.array_equal(np.isfinite(fit), fin)
+        scale = 1.0 if metric == "pearson" else np.maximum(np.abs(one[fin]), 1e-6)
+        assert np.all(np.abs(fit[fin] - one[fin]) <= 1e-4 * scale), P
+        check_fitness(fit, ref, sens, flags, metric, label=f"row shards P={P} {metric}")
+
+
+def test_row_shards_constant_programs(gp, pctx, orc):
+    """Closed-form variable-free programs through the shard path (their sums come from the
+    dataset moments W, S_y, S_yy, which are additive over shards too)."""
+    from tests.test_gpu_parity import _constant_heavy_population
+    nodes, off = _constant_heavy_population(120, seed=9)
+    for metric in ("mse", "rmse", "logloss", "pearson"):
+        Xm, ym = _dataset(metric, 30_000, seed=3)
+        w = synth.weights(Xm.shape[1], seed=4)
+        pctx.set_reference_row(Xm[:, 0].copy(), float(ym[0]))
+        one, st1 = pctx.evaluate(dev(nodes), dev(off), dev(Xm), dev(ym), dev(w), metric=metric,
+                                 max_stack=8)
+        tot = _shard_sum(pctx, nodes, off, Xm, ym, w, metric, 4)
+        fit, st = pctx.finalize_sums(dev(nodes), dev(off), torch.from_numpy(tot).cuda(),
+                                     Xm.shape[0], metric=metric, max_stack=8)
+        one, fit = one.cpu().numpy(), fit.cpu().numpy()
+        assert torch.equal(st, st1)
+        fin = np.isfinite(one)
+        scale = 1.0 if metric == "pearson" else np.maximum(np.abs(one[fin]), 1e-6)
+        assert np.all(np.abs(fit[fin] - one[fin]) <= 1e-4 * scale), metric
+        ref, sens, flags = orc.population_fitness(nodes, off, Xm, ym, w, metric)
+        check_fitness(fit, ref, sens, flags, metric, label=f"const shards {metric}")
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_program_chunks_simulated(gp, pctx, orc, oracle_cache, P):
+    """each rank evaluates the programs [r c, (r+1) c), c = ceil(n / P), over all rows
+    (gp_context_set_program_range); the assembled fitness and status are bit-identical to one
+    evaluation of the whole population (the per-program sums do not depend on the group a
+    program shares a work item with)."""
+    X, y, w, nodes, off, ref, sens, flags = _case(orc, oracle_cache, "mse", True)
+    n = len(off) - 1
+    full, stf = pctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), dev(w), metric="mse",
+                              max_stack=8)
+    c = (n + P - 1) // P
+    fit = np.empty(n, np.float32)
+    st = np.empty(n, np.int32)
+    for r in range(P):
+        lo, hi = min(n, r * c), min(n, (r + 1) * c)
+        pctx.set_program_range(lo, hi)
+        f, s = pctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), dev(w), metric="mse",
+                             max_stack=8)
+        fit[lo:hi] = f.cpu().numpy()[lo:hi]
+        st[lo:hi] = s.cpu().numpy()[lo:hi]
+    pctx.set_program_range(0, -1)
+    assert np.array_equal(fit, full.cpu().numpy()) and np.array_equal(st, stf.cpu().numpy())
+
+
+def test_partial_rejects_spearman(gp, pctx):
+    X, y = synth.pagie_grid(16)
+    nodes, off = synth.random_population(8, seed=1, depth=(1, 3), max_stack=8)
+    with pytest.raises(gp.GPError):
+        pctx.evaluate_partial(dev(nodes), dev(off), dev(X), dev(y), metric="spearman",
+                              max_stack=8)
