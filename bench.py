@@ -2,11 +2,21 @@
 """Benchmark of the B200 hot path of arXiv 2110.11226.
 
 Metric (BASELINE.json): GP node-evals/sec and sec/generation at Pagie 16M rows (config C3:
-Pagie-1 on the 4096 x 4096 grid = 16,777,216 rows, population 8192, MSE). One step = one
-gp_generation = the whole hot path of SURVEY section 8(a): tournament selection (GPU), host
-mutation, one H2D copy of the flat population, stage + fused evaluate + reduce (+ all-reduce at
-N > 1) + finalize. value = node evaluations (sum of program lengths x dataset rows, all ranks)
-per second of device time (CUDA events on the engine stream, max over ranks).
+Pagie-1 on the 4096 x 4096 grid = 16,777,216 rows, population 8192, MSE).
+
+One step = one gp_generation from a FIXED population: the engine is reset to the generation-0
+(ramped half-and-half) population and its fitness (gp_engine_set_population, device to device),
+then runs tournament selection, mutation (both on the GPU), compile + fused evaluation +
+reduction (+ all-reduce at N > 1) + finalize of the children -- every row of SURVEY section 8(a) on
+the same workload every step, so the number does not drift with the run length (a free-running
+population collapses under parsimony pressure, see the "evolved" field). value = node evaluations
+(sum of the children's lengths x dataset rows, all ranks) per second of device time (CUDA events on
+the engine stream, max over ranks).
+
+Also reported: "evaluate" (gp_evaluate alone on the generation-0 population, median of >= 10 reps),
+"evolved" (sec/generation of consecutive generations from generation 0), the evaluator roofline,
+the oracle baseline (1 thread and all cores) and the end-to-end number (dataset streamed from
+pinned host memory every step).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c3]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, rows sharded)
@@ -163,23 +173,64 @@ def ncu_traffic():
         return None
 
 
-def cpu_baseline(nodes, off, X, y, metric, max_seconds=20.0):
-    """The oracle (C, double, recursive, single-threaded, as it stands) on a bounded sample:
-    all programs of the final population on the first rows of this rank's shard."""
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _oracle_chunk(job):
+    """Worker of the all-core oracle mode: one contiguous program chunk, single-threaded."""
+    import oracle
+    nodes, off, X, y, metric = job
+    oracle.population_fitness(nodes, off, X, y, None, metric)
+    return float(np.diff(off).sum()) * X.shape[1]
+
+
+def cpu_baseline(nodes, off, X, y, metric, max_seconds=12.0):
+    """The oracle (C, double, recursive, as it stands) on a bounded sample: all programs of the
+    population on the first rows of this rank's shard; 1 thread, then all host cores (processes
+    over program chunks -- the oracle itself is not changed)."""
+    import multiprocessing as mp
+
     import oracle
     oracle.build()
     lens = np.diff(off)
-    n_rows = 256
+    n_rows = 128
     t0 = time.perf_counter()
     oracle.population_fitness(nodes, off, X[:, :n_rows], y[:n_rows], None, metric)
     dt = time.perf_counter() - t0
     rows = int(min(X.shape[1], max(n_rows, n_rows * (max_seconds * 0.5) / max(dt, 1e-6))))
+    Xs, ys = np.ascontiguousarray(X[:, :rows]), np.ascontiguousarray(y[:rows])
     t0 = time.perf_counter()
-    oracle.population_fitness(nodes, off, X[:, :rows], y[:rows], None, metric)
-    dt = time.perf_counter() - t0
-    return {"value": float(lens.sum()) * rows / dt, "unit": "node-evals/s", "cores": 1,
-            "kind": "oracle", "sample": f"all {len(lens)} programs of the final population x "
-                                        f"first {rows} rows ({dt:.1f} s, C double recursive)"}
+    oracle.population_fitness(nodes, off, Xs, ys, None, metric)
+    dt1 = time.perf_counter() - t0
+    one = float(lens.sum()) * rows / dt1
+    cores = len(os.sched_getaffinity(0))
+    allc = None
+    if cores > 1:
+        n = len(off) - 1
+        bounds = [n * k // cores for k in range(cores + 1)]
+        jobs = [(nodes[off[a]:off[b]], off[a:b + 1] - off[a], Xs, ys, metric)
+                for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+        try:
+            with mp.get_context("fork").Pool(cores) as pool:
+                t0 = time.perf_counter()
+                work = sum(pool.map(_oracle_chunk, jobs))
+                dta = time.perf_counter() - t0
+            allc = {"value": work / dta, "cores": cores,
+                    "sample": f"same sample, programs split over {cores} processes ({dta:.1f} s)"}
+        except Exception as ex:                       # no fork / no /dev/shm: report why
+            allc = {"value": None, "cores": cores, "error": str(ex)[:200]}
+    return {"value": one, "unit": "node-evals/s", "cores": 1, "kind": "oracle",
+            "cpu_model": _cpu_model(), "host_cores": cores,
+            "sample": f"all {len(lens)} programs of the step's children x first {rows} rows "
+                      f"({dt1:.1f} s, C double recursive, 1 thread)",
+            "all_cores": allc}
 
 
 def run_b200(args, cfg):
@@ -215,19 +266,32 @@ def run_b200(args, cfg):
     y = torch.from_numpy(yh).cuda(local)
     torch.cuda.synchronize()
     kw = dict(population_size=cfg["pop"], metric=cfg["metric"], seed=2110,
-              init_depth_min=cfg["depth"][0], init_depth_max=cfg["depth"][1])
+              init_depth_min=cfg["depth"][0], init_depth_max=cfg["depth"][1],
+              device_mutation=0 if args.host_mutation else 1)
     eng = gp.Engine(ctx, X, y, **kw)
     st0 = eng.init_population()
-    n0, o0, _ = eng.population()
-    gen0 = (n0, o0, st0["op_count"], st0["const_programs"])
-    for _ in range(args.warmup):
-        eng.generation()
+    g0n, g0o, g0f = eng.population_device()        # the fixed starting population (HBM)
+    n0_len = int(g0n.shape[0])
+    rows_local = X.shape[1] / (world if by_prog else 1)
+
+    def step(e):
+        e.set_population(g0n, g0o, g0f, generation=0)
+        return e.generation()
 
     def barrier():
         if world > 1:
             dist.barrier(device_ids=[local])
 
-    # ---- timed region: K generations, inputs resident in HBM -----------------------------------
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(v) for v in t]
+
+    for _ in range(args.warmup):
+        step(eng)
+
+    # ---- timed region: K steps, inputs resident in HBM ---------------------------------------
     ctx.set_profiling(True)
     ctx.eval_timing(reset=True)
     ctx.kernel_launches(reset=True)
@@ -238,7 +302,7 @@ def run_b200(args, cfg):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            steps.append(eng.generation())
+            steps.append(step(eng))
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -246,64 +310,83 @@ def run_b200(args, cfg):
     eval_ms, eval_launches = ctx.eval_timing(reset=True)
     launches = ctx.kernel_launches(reset=True)
     ctx.set_profiling(False)
+    ms, eval_ms = max_over_ranks([ms, eval_ms])
     node_evals = sum(s["total_nodes"] for s in steps) * m_global
-    t = torch.tensor([ms, eval_ms], dtype=torch.float64, device=f"cuda:{local}")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, eval_ms_max = float(t[0]), float(t[1])
     value = node_evals / (ms * 1e-3)
-
-    # roofline of the dominant kernel (the fused evaluator), this rank's launches: algorithmic
-    # per-row work = variable-dependent nodes only (variable-free subtrees are constants)
-    # this rank's share of the per-row work: its row shard, or (program sharding) all rows x about
-    # 1 / world of the programs
-    rows_local = X.shape[1] / (world if by_prog else 1)
     sfu = fp32 = 0
     for s in steps:
         a, b2 = algorithmic_ops(s["op_count"], rows_local, cfg["metric"], cfg["pop"],
                                 0 if args.no_const_programs else s["const_programs"])
         sfu, fp32 = sfu + a, fp32 + b2
     roofline = roofline_of(sfu, fp32, eval_ms, eval_launches, ms, traffic=args.config == "c3")
-    var_nodes = sum(sum(s["op_count"]) for s in steps) * m_global
-    const_share = float(np.mean([s["const_nodes"] / max(1, s["total_nodes"]) for s in steps]))
 
-    # the same kernel on the generation-0 (ramped half-and-half) population, which carries far
-    # more per-row transcendental work than evolved populations: a capability point
-    roof0 = None
-    if gen0 is not None:
-        n0, o0, ops0, cp0 = gen0
-        nd, of = torch.from_numpy(n0).cuda(local), torch.from_numpy(o0).cuda(local)
-        fit_buf = torch.empty(len(o0) - 1, dtype=torch.float32, device=f"cuda:{local}")
-        for _ in range(2):
-            ctx.evaluate(nd, of, X, y, metric=cfg["metric"], max_stack=20, fitness_out=fit_buf)
+    # ---- gp_evaluate alone on the fixed generation-0 population (SURVEY D definition) -----------
+    fit_buf = torch.empty(cfg["pop"], dtype=torch.float32, device=f"cuda:{local}")
+    for _ in range(2):
+        ctx.evaluate(g0n, g0o, X, y, metric=cfg["metric"], max_stack=20, fitness_out=fit_buf)
+    torch.cuda.synchronize()
+    reps = max(10, args.eval_reps)
+    times = []
+    ctx.set_profiling(True)
+    ctx.eval_timing(reset=True)
+    for _ in range(reps):
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        ctx.evaluate(g0n, g0o, X, y, metric=cfg["metric"], max_stack=20, fitness_out=fit_buf)
+        a1.record(stream)
         torch.cuda.synchronize()
-        ctx.set_profiling(True)
-        ctx.eval_timing(reset=True)
-        reps = 5
-        for _ in range(reps):
-            ctx.evaluate(nd, of, X, y, metric=cfg["metric"], max_stack=20, fitness_out=fit_buf)
-        torch.cuda.synchronize()
-        ms0, l0 = ctx.eval_timing(reset=True)
-        ctx.set_profiling(False)
-        a0, b0 = algorithmic_ops(ops0, rows_local, cfg["metric"], cfg["pop"],
-                                 0 if args.no_const_programs else cp0)
-        roof0 = roofline_of(a0 * reps, b0 * reps, ms0, l0, ms0, traffic=args.config == "c3")
-        roof0["node_evals_per_s"] = float(len(n0)) * rows_local * reps / (ms0 * 1e-3)
-        roof0["population"] = "generation 0 (ramped half-and-half), mean length %.2f" % (
-            len(n0) / (len(o0) - 1))
+        times.append(max_over_ranks([a0.elapsed_time(a1)])[0])
+    k_ms, k_l = ctx.eval_timing(reset=True)
+    ctx.set_profiling(False)
+    t_med = statistics.median(times)
+    a0_, b0_ = algorithmic_ops(st0["op_count"], rows_local, cfg["metric"], cfg["pop"],
+                               0 if args.no_const_programs else st0["const_programs"])
+    roof0 = roofline_of(a0_ * reps, b0_ * reps, k_ms, k_l, k_ms, traffic=False)
+    evaluate = {"population": "generation 0 (ramped half-and-half), mean length %.2f"
+                              % (n0_len / cfg["pop"]),
+                "reps": reps, "median_ms": round(t_med, 3), "min_ms": round(min(times), 3),
+                "max_ms": round(max(times), 3),
+                "node_evals_per_s": n0_len * m_global / (t_med * 1e-3),
+                "row_program_evals_per_s": cfg["pop"] * m_global / (t_med * 1e-3),
+                "t_eval_scope": "gp_evaluate call: compile, evaluator, reduction, "
+                                "all-reduce (N > 1), finalize (CUDA events, max over ranks)",
+                "roofline": roof0}
 
-    # ---- end-to-end: dataset streamed from pinned host memory every step ------------------------
+    # ---- evolved: consecutive generations from generation 0 (the population drifts) -----------
+    evolved = None
+    if not args.no_evolved:
+        eng.set_population(g0n, g0o, g0f, generation=0)
+        ev_steps, ev_ms = [], []
+        for _ in range(args.evolved_gens):
+            barrier()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            ev_steps.append(eng.generation())
+            b1.record(stream)
+            torch.cuda.synchronize()
+            ev_ms.append(max_over_ranks([b0.elapsed_time(b1)])[0])
+        tot = sum(ev_ms)
+        evolved = {
+            "generations": args.evolved_gens,
+            "sec_per_generation_median": statistics.median(ev_ms) / 1e3,
+            "nominal_node_evals_per_s": sum(s["total_nodes"] for s in ev_steps) * m_global / (tot * 1e-3),
+            "var_node_evals_per_s": sum(sum(s["op_count"]) for s in ev_steps) * m_global / (tot * 1e-3),
+            "mean_program_length_last": ev_steps[-1]["total_nodes"] / cfg["pop"],
+            "const_node_share_last": round(ev_steps[-1]["const_nodes"] / max(1, ev_steps[-1]["total_nodes"]), 4),
+            "const_program_share_last": round(ev_steps[-1]["const_programs"] / cfg["pop"], 4),
+            "note": "nominal counts every node x row, incl. variable-free subtrees folded at compile "
+                    "time and closed-form constant programs; var_node_evals counts only "
+                    "variable-dependent nodes"}
+
+    # ---- end-to-end: dataset streamed from pinned host memory every step -----------------------
     e2e = None
     if not args.no_e2e:
         Xp = torch.from_numpy(Xh).pin_memory()
         yp = torch.from_numpy(yh).pin_memory()
-        pop_bytes = 0
-        # a fresh engine with the same seed replays the SAME generations as the timed region
-        # (the engine is deterministic), so value and e2e price identical populations
-        eng = gp.Engine(ctx, X, y, **kw)
-        eng.init_population()
-        for _ in range(args.warmup):
-            eng.generation()
+        for _ in range(2):
+            eng.set_dataset(Xp, yp)
+            step(eng)
         barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -311,44 +394,51 @@ def run_b200(args, cfg):
         e2e_steps = []
         for _ in range(args.steps):
             eng.set_dataset(Xp, yp)
-            e2e_steps.append(eng.generation())
+            e2e_steps.append(step(eng))
         f1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ms2 = f0.elapsed_time(f1)
-        t2 = torch.tensor([ms2], dtype=torch.float64, device=f"cuda:{local}")
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        ms2 = float(t2[0])
-        pop_bytes = sum(s["total_nodes"] * 8 + (cfg["pop"] + 1) * 8 for s in e2e_steps) / len(e2e_steps)
+        ms2 = max_over_ranks([f0.elapsed_time(f1)])[0]
+        # per step the engine reads back the child node total (8 B), tournament count and error
+        # word (4 + 4 B) and the statistics record (op histogram, best, mean); the host mutation
+        # path also copies the population and reads fitness + winners
+        dev_mut = not args.host_mutation
+        d2h = 16 + 280 if dev_mut else int(cfg["pop"] * 4 + 2 * cfg["pop"] * 4)
+        h2d_pop = 0 if dev_mut else int(np.mean([s["total_nodes"] for s in e2e_steps]) * 8 + (cfg["pop"] + 1) * 8)
         e2e = {"value": sum(s["total_nodes"] for s in e2e_steps) * m_global / (ms2 * 1e-3),
                "unit": "node-evals/s",
-               "h2d_bytes_per_step": int(Xh.nbytes + yh.nbytes + pop_bytes),
-               "d2h_bytes_per_step": int(cfg["pop"] * 4 + np.mean([s["n_tournaments"] for s in e2e_steps]) * 4),
+               "h2d_bytes_per_step": int(Xh.nbytes + yh.nbytes + h2d_pop),
+               "d2h_bytes_per_step": int(d2h),
                "ms_per_step": round(ms2 / args.steps, 3)}
+        eng.set_dataset(X, y)
 
     out = None
     if rank == 0:
         nodes, off, _ = eng.population()
-        if args.dump_population:
-            np.savez_compressed(args.dump_population, nodes=nodes, off=off)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
+            eng.set_population(g0n, g0o, g0f, generation=0)
+            eng.generation()                              # the step's children
+            nodes, off, _ = eng.population()
             cpu = cpu_baseline(nodes, off, Xh, yh, cfg["metric"])
         mean_len = float(np.mean([s["total_nodes"] for s in steps])) / cfg["pop"]
         out = {
             "metric": METRIC, "value": value, "unit": "node-evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "sec_per_generation": ms / args.steps / 1e3,
-            "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, DESIGN.md recipe)",
             "config": {"workload": cfg["workload"], "rows": m_global, "population": cfg["pop"],
                        "metric": cfg["metric"], "mean_program_length": round(mean_len, 3),
+                       "step": "gp_generation from the fixed generation-0 population (reset every "
+                               "step): GPU selection + mutation, evaluation of the children",
+                       "mutation": "host" if args.host_mutation else "device (SURVEY F2)",
                        "parallelism": (f"programs sharded over {world} GPU(s), fitness all-gathered"
                                        if by_prog else f"rows sharded over {world} GPU(s)"),
                        "l2": "inputs larger than L2 (X + y = %.0f MB)" % ((Xh.nbytes + yh.nbytes) * world / 1e6)},
-            "roofline": roofline, "roofline_gen0": roof0,
-            "var_node_evals_per_s": var_nodes / (ms * 1e-3), "const_node_share": round(const_share, 4),
+            "roofline": roofline, "evaluate": evaluate, "evolved": evolved,
+            "var_node_evals_per_s": sum(sum(s["op_count"]) for s in steps) * m_global / (ms * 1e-3),
+            "const_node_share": round(float(np.mean([s["const_nodes"] / max(1, s["total_nodes"]) for s in steps])), 4),
             "const_program_share": round(float(np.mean([s["const_programs"] / cfg["pop"] for s in steps])), 4),
             "const_programs_closed_form": (not args.no_const_programs) and cfg["metric"] in CLOSED_FORM_METRICS,
             "cpu_baseline": cpu, "e2e": e2e,
@@ -365,8 +455,9 @@ def run_b200(args, cfg):
 
 
 def run_reference(args, cfg):
-    """--impl reference: the oracle (C evaluation + Python engine replay) on the host cores,
-    each step one generation of the same workload on a bounded row sample."""
+    """--impl reference: the oracle (C evaluation + Python engine replay) on the host cores, each
+    step the same step as the b200 arm -- one generation from the fixed generation-0 population --
+    with the children evaluated on a bounded row sample."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return None
@@ -378,31 +469,32 @@ def run_reference(args, cfg):
     Xs, ys = np.ascontiguousarray(Xh[:, :sample]), np.ascontiguousarray(yh[:sample])
     ocfg = oe.Config(population_size=cfg["pop"], metric=cfg["metric"], seed=2110,
                      init_depth=cfg["depth"], n_features=Xh.shape[0])
-    pop = oe.ramped_init(ocfg)
-    nodes, off = oe.flatten(pop)
-    fit, _, _ = oracle.population_fitness(nodes, off, Xs, ys, None, cfg["metric"])
+    pop0 = oe.ramped_init(ocfg)
+    nodes, off = oe.flatten(pop0)
+    fit0, _, _ = oracle.population_fitness(nodes, off, Xs, ys, None, cfg["metric"])
     hb = cfg["metric"] == "pearson"
     total = 0.0
     evals = 0
-    for step in range(args.warmup + args.steps):
+    for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        rec = oe.next_generation(pop, fit.astype(np.float32), ocfg, step + 1, hb)
-        pop = rec.population
-        nodes, off = oe.flatten(pop)
-        fit, _, _ = oracle.population_fitness(nodes, off, Xs, ys, None, cfg["metric"])
+        rec = oe.next_generation(pop0, fit0.astype(np.float32), ocfg, 1, hb)
+        nodes, off = oe.flatten(rec.population)
+        oracle.population_fitness(nodes, off, Xs, ys, None, cfg["metric"])
         dt = time.perf_counter() - t0
-        if step >= args.warmup:
+        if k >= args.warmup:
             total += dt
             evals += int(np.diff(off).sum()) * sample
     value = evals / total
     return {"metric": METRIC, "value": value, "unit": "node-evals/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-            "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, DESIGN.md recipe)",
             "impl": "reference",
             "config": {"workload": cfg["workload"], "rows": m, "population": cfg["pop"],
-                       "metric": cfg["metric"], "parallelism": "host, 1 thread"},
+                       "metric": cfg["metric"], "parallelism": "host, 1 thread",
+                       "step": "one generation from the fixed generation-0 population"},
             "cpu_baseline": {"value": value, "unit": "node-evals/s", "cores": 1, "kind": "oracle",
+                             "cpu_model": _cpu_model(),
                              "sample": f"each step: one generation (oracle select + mutate + "
                                        f"evaluate) with evaluation on the first {sample} rows"},
             "e2e": {"value": value, "unit": "node-evals/s", "h2d_bytes_per_step": 0,
@@ -416,22 +508,29 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--weak", action="store_true", help="per-GPU rows fixed (default: strong)")
+    ap.add_argument("--pop", type=int, default=None, help="population size override (C5 sweep)")
+    ap.add_argument("--eval-reps", type=int, default=10)
+    ap.add_argument("--evolved-gens", type=int, default=10)
+    ap.add_argument("--no-evolved", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--host-mutation", action="store_true",
+                    help="mutate on the host (P:237) instead of the GPU (SURVEY F2)")
     ap.add_argument("--shard", default="rows", choices=["rows", "programs"],
                     help="multi-GPU split: row shards + partial-sum all-reduce (default) or "
                          "program chunks + fitness all-gather (SURVEY F3)")
     ap.add_argument("--no-const-programs", action="store_true",
                     help="evaluate variable-free programs per row (no closed-form fitness)")
-    ap.add_argument("--dump-population", default=None,
-                    help="save the final population (nodes, offsets) to this .npz (analysis)")
     ap.add_argument("--nccl", action="store_true",
                     help="use the NCCL communicator path even with one rank (plumbing check)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.pop:
+        cfg["pop"] = args.pop
+        cfg["workload"] = cfg["workload"].replace(f"population {CONFIGS[args.config]['pop']}",
+                                                  f"population {args.pop}")
     out = run_reference(args, cfg) if args.impl == "reference" else run_b200(args, cfg)
     if out is not None:
         print(json.dumps(out))

@@ -24,6 +24,7 @@
 #ifndef GP_B200_GP_H
 #define GP_B200_GP_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -103,6 +104,9 @@ const char* gp_status_string(gp_status s);
 const char* gp_last_error(const gp_context* ctx);
 /* Library version string, e.g. "gp_b200 0.1 sm_100a". */
 const char* gp_version(void);
+/* Copies `bytes` between any two [host|device] buffers (cudaMemcpyDefault) [sync]; lets a binding
+ * take copies of the borrowed device views below without a second CUDA runtime. */
+gp_status gp_device_copy(void* dst, const void* src, size_t bytes);
 
 /* ---------------------------------------------------------------------------------------------
  * Context: device, stream, optional NCCL communicator (data parallelism over dataset rows).
@@ -267,7 +271,8 @@ gp_status gp_tournament_select(gp_context* ctx, const float* fitness, const int6
                                uint32_t generation, int32_t* winners_out);
 
 /* ---------------------------------------------------------------------------------------------
- * Engine: the generational loop of Alg. 1 with host mutations.
+ * Engine: the generational loop of Alg. 1; mutations on the GPU or the
+ * host.
  * -------------------------------------------------------------------------------------------*/
 typedef struct {
   int32_t population_size;     /* Table 2: 50, Table 6: 35 */
@@ -286,7 +291,10 @@ typedef struct {
   int32_t function_set[32];    /* opcodes; Table 2 / 6: {add, sub, mul, div, sin, cos, tan} */
   int32_t stack_capacity;      /* depth <= stack_capacity - 1, <= GP_MAX_STACK */
   uint64_t seed;               /* Philox key for init, kinds, tournaments and mutations */
-  int32_t n_threads;           /* host threads for mutation (0 = all cores) */
+  int32_t n_threads;           /* host threads for the host mutation path (0 = cores / ranks) */
+  int32_t device_mutation;     /* 1 (default): kinds, mutations and the flat population stay on the
+                                  GPU (mutate.cu; needs init_depth_max <= 10, else the
+                                  host path runs); 0: host mutation + one H2D copy */
 } gp_config;
 
 /* Fills Table 6's parameters with SPEC defaults for the rest. */
@@ -321,13 +329,28 @@ gp_status gp_engine_set_dataset(gp_engine* e, const float* X, int64_t ldx, const
 gp_status gp_engine_destroy(gp_engine* e);
 /* Alg. 1 lines 2-3: ramped half-and-half init and evaluation. [sync] */
 gp_status gp_engine_init_population(gp_engine* e, gp_generation_stats* stats_out);
-/* Alg. 1 lines 5-8 once: kinds, tournaments, host mutations, one H2D copy of
- * the flat population, evaluation. [sync] */
+/* Alg. 1 lines 5-8 once: kinds, tournaments, mutations, evaluation. With
+ * device_mutation the whole step runs on the GPU (two small D2H reads: the child node total,
+ * then the statistics); otherwise mutations run on the host followed by one H2D copy of the flat
+ * population. Both paths produce bit-identical populations. [sync] */
 gp_status gp_generation(gp_engine* e, gp_generation_stats* stats_out);
 /* Borrowed [host] views of the current population and its fp32 raw fitness; valid until the
- * next gp_generation / gp_engine_init_population / gp_engine_destroy. */
+ * next gp_generation / gp_engine_init_population / gp_engine_set_population / gp_engine_destroy.
+ * [sync] (with device mutation the population is copied from HBM on this call). */
 gp_status gp_engine_population(gp_engine* e, const gp_node** nodes, const int64_t** offsets,
                                const float** fitness, int32_t* n_programs, int64_t* n_nodes);
+/* Borrowed DEVICE views of the current population (flat CSR) and its fitness, same validity. */
+gp_status gp_engine_population_device(gp_engine* e, const gp_node** nodes,
+                                      const int64_t** offsets, const float** fitness,
+                                      int32_t* n_programs, int64_t* n_nodes);
+/* Replaces the current population (cfg.population_size programs, [host|device] flat CSR with
+ * offsets[0] == 0) and declares it generation `generation`. fitness [host|device] fp32[n]: the
+ * population's raw fitness, or NULL to evaluate it now. Programs must be valid with depth <=
+ * stack_capacity - 1 (GP_ERR_ARG otherwise). Used to resume a run, to seed a population, and by
+ * the benchmark to start every step from the same population. [sync] */
+gp_status gp_engine_set_population(gp_engine* e, const gp_node* nodes, const int64_t* offsets,
+                                   int32_t n_programs, int64_t n_nodes, const float* fitness,
+                                   int32_t generation, gp_generation_stats* stats_out);
 /* [host] views of the last generation's mutation kinds (0 crossover, 1 subtree, 2 hoist,
  * 3 point, 4 reproduction) and tournament winners (for replay tests). */
 gp_status gp_engine_last_selection(gp_engine* e, const int32_t** kinds, const int32_t** winners,

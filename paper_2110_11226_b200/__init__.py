@@ -13,6 +13,7 @@ var index or float32 bits of the constant) and ``offsets`` int64 ``(n_programs +
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import numpy as np
 
@@ -104,9 +105,12 @@ class Context:
         _check(lib().gp_context_create(ctypes.byref(h), device, ctypes.c_void_p(stream.cuda_stream),
                                        uid, rank, world_size), None, "gp_context_create")
         self.handle = h
+        self._engines = weakref.WeakSet()      # engines on this context (closed first)
 
     def close(self):
         if getattr(self, "handle", None):
+            for e in list(getattr(self, "_engines", ())):
+                e.close()
             lib().gp_context_destroy(self.handle)
             self.handle = None
 
@@ -259,6 +263,7 @@ class Engine:
                                       int(X.stride(0)), _ptr(y), _ptr(w), int(X.shape[1]),
                                       int(X.shape[0])), ctx.handle, "gp_engine_create")
         self.handle = h
+        ctx._engines.add(self)
 
     def set_dataset(self, X, y, w=None):
         self._keep = (X, y, w)
@@ -293,6 +298,36 @@ class Engine:
                                        (n.value,)).copy()
         return nodes_np, off_np, fit_np
 
+    def population_device(self):
+        """Device copies (torch, cuda) of the current population: (nodes (N,2) int32, offsets
+        int64, fitness f32) -- gp_engine_population_device views, cloned."""
+        import torch
+        nodes, off, fit = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        n, nn = ctypes.c_int32(), ctypes.c_int64()
+        _check(lib().gp_engine_population_device(self.handle, ctypes.byref(nodes),
+                                                 ctypes.byref(off), ctypes.byref(fit),
+                                                 ctypes.byref(n), ctypes.byref(nn)),
+               self.ctx.handle, "gp_engine_population_device")
+        dev = torch.device("cuda", self.ctx.device)
+        out_n = torch.empty((nn.value, 2), dtype=torch.int32, device=dev)
+        out_o = torch.empty(n.value + 1, dtype=torch.int64, device=dev)
+        out_f = torch.empty(n.value, dtype=torch.float32, device=dev)
+        torch.cuda.synchronize(dev)
+        for dst, src in ((out_n, nodes), (out_o, off), (out_f, fit)):
+            _check(lib().gp_device_copy(_ptr(dst), src, dst.numel() * dst.element_size()),
+                   self.ctx.handle, "copy")
+        return out_n, out_o, out_f
+
+    def set_population(self, nodes, offsets, fitness=None, generation: int = 0) -> dict:
+        """gp_engine_set_population ([host|device] flat CSR; fitness None = evaluate now)."""
+        self._keep_pop = (nodes, offsets, fitness)
+        st = GpGenerationStats()
+        _check(lib().gp_engine_set_population(self.handle, _ptr(nodes), _ptr(offsets),
+                                              int(offsets.shape[0] - 1), int(nodes.shape[0]),
+                                              _ptr(fitness), int(generation), ctypes.byref(st)),
+               self.ctx.handle, "gp_engine_set_population")
+        return st.as_dict()
+
     def last_selection(self):
         """(kinds int32 [n], winners int32 [T]) of the last gp_generation."""
         k, w = ctypes.c_void_p(), ctypes.c_void_p()
@@ -308,9 +343,9 @@ class Engine:
         return kinds, winners
 
     def close(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and getattr(self.ctx, "handle", None):
             lib().gp_engine_destroy(self.handle)
-            self.handle = None
+        self.handle = None
 
     def __del__(self):
         try:

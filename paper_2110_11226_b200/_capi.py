@@ -47,6 +47,10 @@ SIGNATURES = {
     "gp_generation": ([P, P], ctypes.c_int),
     "gp_engine_population": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
                               ctypes.POINTER(i32), ctypes.POINTER(i64)], ctypes.c_int),
+    "gp_engine_population_device": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
+                                     ctypes.POINTER(i32), ctypes.POINTER(i64)], ctypes.c_int),
+    "gp_engine_set_population": ([P, P, P, i32, i64, P, i32, P], ctypes.c_int),
+    "gp_device_copy": ([P, P, ctypes.c_size_t], ctypes.c_int),
     "gp_engine_last_selection": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i32)],
                                  ctypes.c_int),
 }
@@ -59,7 +63,7 @@ class GpConfig(ctypes.Structure):
         ("p_crossover", f64), ("p_subtree", f64), ("p_hoist", f64), ("p_point", f64),
         ("p_point_replace", f64), ("init_depth_min", i32), ("init_depth_max", i32),
         ("const_lo", f32), ("const_hi", f32), ("n_functions", i32), ("function_set", i32 * 32),
-        ("stack_capacity", i32), ("seed", u64), ("n_threads", i32),
+        ("stack_capacity", i32), ("seed", u64), ("n_threads", i32), ("device_mutation", i32),
     ]
 
 

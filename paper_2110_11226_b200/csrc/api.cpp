@@ -229,7 +229,14 @@ const char* gp_last_error(const gp_context* ctx) {
   return ctx ? ctx->err.c_str() : g_last_global_error.c_str();
 }
 
-const char* gp_version(void) { return "gp_b200 0.1 sm_100a"; }
+const char* gp_version(void) { return "gp_b200 0.2 sm_100a"; }
+
+gp_status gp_device_copy(void* dst, const void* src, size_t bytes) {
+  if ((!dst || !src) && bytes) return GP_ERR_ARG;
+  cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
+  if (e != cudaSuccess) { g_last_global_error = cudaGetErrorString(e); return GP_ERR_CUDA; }
+  return GP_OK;
+}
 
 gp_status gp_get_unique_id(void* out_id) {
   if (!out_id) return GP_ERR_ARG;

@@ -26,6 +26,7 @@
 
 #include "common.h"
 #include "gp_internal.h"
+#include "mutate.h"
 
 using namespace gpb;
 
@@ -307,11 +308,23 @@ struct gp_engine {
   StageBuf d_nodes, d_off, d_fit, d_win, d_status;
   int64_t n_nodes = 0;
   std::vector<int32_t> kinds, winners;
+  // device mutation (mutate.cu): the population lives in d_nodes / d_off; the next
+  // generation is built in d_nodes2 / d_off2 and swapped in
+  bool dev_mut = false;
+  bool host_view_valid = true;   // h_nodes / h_off / fit mirror the current population
+  int32_t last_T = 0;            // tournaments of the last generation (device path)
+  StageBuf d_nodes2, d_off2, d_kinds, d_tcnt, d_toff, d_recipe, d_len, d_depth, d_stats;
+  DevGenStats* h_stats = nullptr;  // pinned
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
   ~gp_engine() {
     if (h_nodes) cudaFreeHost(h_nodes);
     if (h_off) cudaFreeHost(h_off);
-    for (StageBuf* b : {&d_nodes, &d_off, &d_fit, &d_win, &d_status})
+    if (h_stats) cudaFreeHost(h_stats);
+    for (cudaEvent_t x : ev)
+      if (x) cudaEventDestroy(x);
+    for (StageBuf* b : {&d_nodes, &d_off, &d_fit, &d_win, &d_status, &d_nodes2, &d_off2, &d_kinds,
+                        &d_tcnt, &d_toff, &d_recipe, &d_len, &d_depth, &d_stats})
       if (b->p) cudaFree(b->p);
     if (own_X) cudaFree(own_X);
     if (own_y) cudaFree(own_y);
@@ -364,7 +377,7 @@ struct gp_engine {
 
   // Flatten pop into pinned CSR, copy to HBM (one copy each for nodes and offsets), evaluate,
   // read back fitness.
-  gp_status evaluate(gp_generation_stats* stats) {
+  gp_status evaluate(gp_generation_stats* stats, const float* given_fitness = nullptr) {
     const int n = (int)pop.size();
     double t0 = now_s();
     int64_t total = 0;
@@ -429,9 +442,15 @@ struct gp_engine {
     if ((s = ctx->cuda(cudaMemcpyAsync(d_nodes.p, h_nodes, (size_t)total * sizeof(gp_node), cudaMemcpyHostToDevice, ctx->stream), "H2D nodes"))) return s;
     if ((s = ctx->cuda(cudaMemcpyAsync(d_off.p, h_off, (size_t)(n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream), "H2D offsets"))) return s;
     double t1 = now_s();
-    s = gp_evaluate(ctx, (const gp_node*)d_nodes.p, (const int64_t*)d_off.p, n, total,
-                    std::min(max_need, GP_MAX_STACK), X, ldx, y, w, n_rows, n_cols,
-                    (gp_metric)cfg.metric, (float*)d_fit.p, (uint32_t*)d_status.p);
+    host_view_valid = true;
+    if (given_fitness) {                 // gp_engine_set_population with known fitness
+      s = ctx->cuda(cudaMemcpyAsync(d_fit.p, given_fitness, (size_t)n * sizeof(float),
+                                    cudaMemcpyDefault, ctx->stream), "fitness copy");
+    } else {
+      s = gp_evaluate(ctx, (const gp_node*)d_nodes.p, (const int64_t*)d_off.p, n, total,
+                      std::min(max_need, GP_MAX_STACK), X, ldx, y, w, n_rows, n_cols,
+                      (gp_metric)cfg.metric, (float*)d_fit.p, (uint32_t*)d_status.p);
+    }
     if (s) return s;
     fit.resize(n);
     if ((s = ctx->cuda(cudaMemcpyAsync(fit.data(), d_fit.p, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream), "D2H fitness"))) return s;
@@ -441,6 +460,177 @@ struct gp_engine {
       stats->t_h2d_s += t1 - t0;
       stats->t_eval_s += t2 - t1;
     }
+    return GP_OK;
+  }
+
+  MutConfig mut_config() const {
+    MutConfig m{};
+    m.k0 = (uint32_t)cfg.seed;
+    m.k1 = (uint32_t)(cfg.seed >> 32);
+    m.n_features = n_cols;
+    m.n_functions = cfg.n_functions;
+    for (int i = 0; i < 32; ++i) m.function_set[i] = cfg.function_set[i];
+    m.const_lo = cfg.const_lo;
+    m.const_hi = cfg.const_hi;
+    m.p[0] = cfg.p_crossover;
+    m.p[1] = cfg.p_subtree;
+    m.p[2] = cfg.p_hoist;
+    m.p[3] = cfg.p_point;
+    m.p_point_replace = cfg.p_point_replace;
+    m.init_depth_min = cfg.init_depth_min;
+    m.init_depth_max = cfg.init_depth_max;
+    m.stack_capacity = cfg.stack_capacity;
+    return m;
+  }
+
+  gp_status dev_buffers(int n) {
+    gp_status s;
+    if ((s = ctx->grow(&d_kinds.p, &d_kinds.cap, (size_t)n * 4, "kinds"))) return s;
+    if ((s = ctx->grow(&d_tcnt.p, &d_tcnt.cap, (size_t)n * 4, "tcount"))) return s;
+    if ((s = ctx->grow(&d_toff.p, &d_toff.cap, (size_t)(n + 1) * 4, "toff"))) return s;
+    if ((s = ctx->grow(&d_win.p, &d_win.cap, (size_t)2 * n * 4, "winners"))) return s;
+    if ((s = ctx->grow(&d_recipe.p, &d_recipe.cap, (size_t)n * sizeof(Recipe), "recipes"))) return s;
+    if ((s = ctx->grow(&d_len.p, &d_len.cap, (size_t)n * 4, "lens"))) return s;
+    if ((s = ctx->grow(&d_off2.p, &d_off2.cap, (size_t)(n + 1) * 8, "off2"))) return s;
+    if ((s = ctx->grow(&d_depth.p, &d_depth.cap, (size_t)n * 4, "depth"))) return s;
+    if ((s = ctx->grow(&d_stats.p, &d_stats.cap, sizeof(DevGenStats), "stats"))) return s;
+    if (!h_stats && cudaMallocHost(&h_stats, sizeof(DevGenStats)) != cudaSuccess)
+      return ctx->fail(GP_ERR_OOM, "pinned stats");
+    for (cudaEvent_t& x : ev)
+      if (!x && cudaEventCreate(&x) != cudaSuccess) return ctx->fail(GP_ERR_CUDA, "event");
+    return GP_OK;
+  }
+
+  // Statistics of the device population + fitness (pop_stats, fit_stats) -> h_stats [sync].
+  gp_status dev_stats(int n) {
+    gp_status s;
+    DevGenStats* ds = (DevGenStats*)d_stats.p;
+    if ((s = ctx->cuda(cudaMemsetAsync(ds, 0, sizeof(DevGenStats), ctx->stream), "stats memset"))) return s;
+    if ((s = ctx->launch(launch_pop_stats((const gp_node*)d_nodes.p, (const int64_t*)d_off.p, n,
+                                          (int32_t*)d_depth.p, ds, ctx->stream), "pop stats"))) return s;
+    if ((s = ctx->launch(launch_fit_stats((const float*)d_fit.p, n, higher ? 1 : 0,
+                                          (const int64_t*)d_off.p, (const int32_t*)d_depth.p, ds,
+                                          ctx->stream), "fit stats"))) return s;
+    if ((s = ctx->cuda(cudaMemcpyAsync(h_stats, ds, sizeof(DevGenStats), cudaMemcpyDeviceToHost, ctx->stream), "D2H stats"))) return s;
+    return ctx->cuda(cudaStreamSynchronize(ctx->stream), "stats sync");
+  }
+
+  void fill_stats_dev(gp_generation_stats* st) {
+    const DevGenStats& d = *h_stats;
+    st->generation = generation;
+    st->best_index = d.best;
+    st->mean_raw = d.mean;
+    st->total_nodes = n_nodes;
+    max_need = std::max(1, d.max_need);
+    st->max_stack_need = max_need;
+    std::copy(d.op_count, d.op_count + GP_OP_COUNT, st->op_count);
+    std::copy(d.op_count, d.op_count + GP_OP_COUNT, op_count);
+    st->const_nodes = const_nodes = d.const_nodes;
+    st->const_programs = const_programs = d.const_programs;
+    if (d.best >= 0) {
+      const float pen = cfg.parsimony * (float)d.best_len;
+      st->best_raw = d.best_raw;
+      st->best_adjusted = higher ? d.best_raw - pen : d.best_raw + pen;
+      st->best_len = d.best_len;
+      st->best_depth = d.best_depth;
+    } else {
+      st->best_raw = st->best_adjusted = NAN;
+      st->best_len = st->best_depth = 0;
+    }
+  }
+
+  // Copies the device population + fitness into the pinned host mirror (host views) [sync].
+  gp_status sync_host_view() {
+    if (host_view_valid) return GP_OK;
+    const int n = cfg.population_size;
+    if ((size_t)n_nodes > h_nodes_cap) {
+      if (h_nodes) cudaFreeHost(h_nodes);
+      h_nodes_cap = (size_t)n_nodes + n_nodes / 2 + 1024;
+      if (cudaMallocHost(&h_nodes, h_nodes_cap * sizeof(gp_node)) != cudaSuccess) return ctx->fail(GP_ERR_OOM, "pinned nodes");
+    }
+    if ((size_t)n + 1 > h_off_cap) {
+      if (h_off) cudaFreeHost(h_off);
+      h_off_cap = (size_t)n + 1;
+      if (cudaMallocHost(&h_off, h_off_cap * sizeof(int64_t)) != cudaSuccess) return ctx->fail(GP_ERR_OOM, "pinned offsets");
+    }
+    fit.resize(n);
+    gp_status s;
+    if ((s = ctx->cuda(cudaMemcpyAsync(h_nodes, d_nodes.p, (size_t)n_nodes * sizeof(gp_node), cudaMemcpyDeviceToHost, ctx->stream), "D2H nodes"))) return s;
+    if ((s = ctx->cuda(cudaMemcpyAsync(h_off, d_off.p, (size_t)(n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream), "D2H offsets"))) return s;
+    if ((s = ctx->cuda(cudaMemcpyAsync(fit.data(), d_fit.p, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream), "D2H fitness"))) return s;
+    if ((s = ctx->cuda(cudaStreamSynchronize(ctx->stream), "host view sync"))) return s;
+    host_view_valid = true;
+    return GP_OK;
+  }
+
+  // One generation on the GPU: kinds -> tournaments -> plan -> [read the child node
+  // total] -> emit -> evaluate -> statistics [read once]. Bit-identical to the host path.
+  gp_status device_generation(gp_generation_stats* st_out) {
+    const int n = cfg.population_size;
+    const uint32_t g = (uint32_t)(generation + 1);
+    const double t0 = now_s();
+    gp_status s;
+    if ((s = dev_buffers(n))) return s;
+    const MutConfig mc = mut_config();
+    cudaStream_t str = ctx->stream;
+    DevGenStats* ds = (DevGenStats*)d_stats.p;
+    cudaEventRecord(ev[0], str);
+    if ((s = ctx->cuda(cudaMemsetAsync(&ds->err, 0, sizeof(int32_t), str), "err memset"))) return s;
+    if ((s = ctx->launch(launch_kinds(n, g, mc, (int32_t*)d_kinds.p, (int32_t*)d_tcnt.p,
+                                      (int32_t*)d_toff.p, str), "kinds"))) return s;
+    ctx->kernel_launches += 1;                     // kinds + scan
+    // tournament t depends only on t: launching the upper bound 2 n gives the same first T
+    if ((s = gp_tournament_select(ctx, (const float*)d_fit.p, (const int64_t*)d_off.p, n, 2 * n,
+                                  cfg.tournament_size, cfg.parsimony, higher ? 1 : 0, cfg.seed, g,
+                                  (int32_t*)d_win.p))) return s;
+    if ((s = ctx->launch(launch_plan((const gp_node*)d_nodes.p, (const int64_t*)d_off.p, n, g, mc,
+                                     (const int32_t*)d_kinds.p, (const int32_t*)d_toff.p,
+                                     (const int32_t*)d_win.p, (Recipe*)d_recipe.p,
+                                     (int32_t*)d_len.p, (int64_t*)d_off2.p, &ds->err, str),
+                         "plan"))) return s;
+    ctx->kernel_launches += 1;                     // plan + scan
+    // the child node total sizes the next buffers and the evaluation (one small D2H)
+    int64_t hdr[2];
+    int32_t T = 0, err = 0;
+    if ((s = ctx->cuda(cudaMemcpyAsync(&hdr[0], (int64_t*)d_off2.p + n, 8, cudaMemcpyDeviceToHost, str), "D2H total"))) return s;
+    if ((s = ctx->cuda(cudaMemcpyAsync(&T, (int32_t*)d_toff.p + n, 4, cudaMemcpyDeviceToHost, str), "D2H T"))) return s;
+    if ((s = ctx->cuda(cudaMemcpyAsync(&err, &ds->err, 4, cudaMemcpyDeviceToHost, str), "D2H err"))) return s;
+    cudaEventRecord(ev[1], str);
+    if ((s = ctx->cuda(cudaStreamSynchronize(str), "plan sync"))) return s;
+    if (err) return ctx->fail(GP_ERR_PROGRAM, "device mutation: program deeper than %d", kMaxDepth);
+    const int64_t total = hdr[0];
+    if ((s = ctx->grow(&d_nodes2.p, &d_nodes2.cap, (size_t)std::max<int64_t>(total, 1) * sizeof(gp_node), "nodes2"))) return s;
+    if ((s = ctx->launch(launch_emit((const gp_node*)d_nodes.p, (const int64_t*)d_off.p, n, g, mc,
+                                     (const Recipe*)d_recipe.p, (const int64_t*)d_off2.p,
+                                     (gp_node*)d_nodes2.p, str), "emit"))) return s;
+    std::swap(d_nodes, d_nodes2);
+    std::swap(d_off, d_off2);
+    n_nodes = total;
+    last_T = T;
+    generation = (int)g;
+    host_view_valid = false;
+    pop.clear();                                   // the host copy is stale from here on
+    cudaEventRecord(ev[2], str);
+    // evaluation (Alg. 1 line 7); every program's depth is <= stack_capacity - 1, so its stack
+    // need is <= stack_capacity
+    if ((s = gp_evaluate(ctx, (const gp_node*)d_nodes.p, (const int64_t*)d_off.p, n, total,
+                         std::min(cfg.stack_capacity, GP_MAX_STACK), X, ldx, y, w, n_rows, n_cols,
+                         (gp_metric)cfg.metric, (float*)d_fit.p, (uint32_t*)d_status.p))) return s;
+    cudaEventRecord(ev[3], str);
+    if ((s = dev_stats(n))) return s;
+    gp_generation_stats st{};
+    float a = 0.f, b = 0.f, c2 = 0.f;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c2, ev[2], ev[3]);
+    st.t_select_s = 1e-3 * a;                      // kinds + tournaments + mutation plans
+    st.t_mutate_s = 1e-3 * b;                      // (node total read) + child emission
+    st.t_h2d_s = 0.0;                              // nothing crosses PCIe
+    st.t_eval_s = 1e-3 * c2;
+    st.n_tournaments = T;
+    fill_stats_dev(&st);
+    st.t_total_s = now_s() - t0;
+    if (st_out) *st_out = st;
     return GP_OK;
   }
 
@@ -500,6 +690,7 @@ void gp_config_default(gp_config* c) {
   c->stack_capacity = GP_MAX_STACK;
   c->seed = 2110;
   c->n_threads = 0;
+  c->device_mutation = 1;          // SURVEY F2 (mutate.cu)
 }
 
 gp_status gp_engine_create(gp_engine** out, gp_context* ctx, const gp_config* cfg, const float* X,
@@ -529,6 +720,8 @@ gp_status gp_engine_create(gp_engine** out, gp_context* ctx, const gp_config* cf
   e->pool.reset(new Pool(std::min(e->threads, 64)));
   gp_status s = e->set_dataset(X, ldx, y, w, n_rows, n_cols);
   if (s) { delete e; return s; }
+  // device mutation needs the generated donors of subtree mutations to fit kMaxDonorNodes
+  e->dev_mut = c.device_mutation != 0 && c.init_depth_max <= kMaxDonorDepth;
   *out = e;
   return GP_OK;
 }
@@ -578,6 +771,7 @@ gp_status gp_generation(gp_engine* e, gp_generation_stats* stats_out) {
   if (!e) return GP_ERR_ARG;
   if (e->generation < 0) return e->ctx->fail(GP_ERR_ARG, "gp_generation before gp_engine_init_population");
   cudaSetDevice(e->ctx->device);
+  if (e->dev_mut) return e->device_generation(stats_out);
   gp_context* ctx = e->ctx;
   const gp_config& c = e->cfg;
   gp_generation_stats st{};
@@ -643,10 +837,25 @@ gp_status gp_generation(gp_engine* e, gp_generation_stats* stats_out) {
 gp_status gp_engine_population(gp_engine* e, const gp_node** nodes, const int64_t** offsets,
                                const float** fitness, int32_t* n_programs, int64_t* n_nodes) {
   if (!e || e->generation < 0) return GP_ERR_ARG;
+  cudaSetDevice(e->ctx->device);
+  gp_status s = e->sync_host_view();
+  if (s) return s;
   if (nodes) *nodes = e->h_nodes;
   if (offsets) *offsets = e->h_off;
   if (fitness) *fitness = e->fit.data();
-  if (n_programs) *n_programs = (int32_t)e->pop.size();
+  if (n_programs) *n_programs = e->cfg.population_size;
+  if (n_nodes) *n_nodes = e->n_nodes;
+  return GP_OK;
+}
+
+gp_status gp_engine_population_device(gp_engine* e, const gp_node** nodes,
+                                      const int64_t** offsets, const float** fitness,
+                                      int32_t* n_programs, int64_t* n_nodes) {
+  if (!e || e->generation < 0) return GP_ERR_ARG;
+  if (nodes) *nodes = (const gp_node*)e->d_nodes.p;
+  if (offsets) *offsets = (const int64_t*)e->d_off.p;
+  if (fitness) *fitness = (const float*)e->d_fit.p;
+  if (n_programs) *n_programs = e->cfg.population_size;
   if (n_nodes) *n_nodes = e->n_nodes;
   return GP_OK;
 }
@@ -654,9 +863,82 @@ gp_status gp_engine_population(gp_engine* e, const gp_node** nodes, const int64_
 gp_status gp_engine_last_selection(gp_engine* e, const int32_t** kinds, const int32_t** winners,
                                    int32_t* n_tournaments) {
   if (!e) return GP_ERR_ARG;
+  if (e->dev_mut && e->generation > 0 && e->d_kinds.p) {
+    cudaSetDevice(e->ctx->device);
+    const int n = e->cfg.population_size;
+    e->kinds.resize(n);
+    e->winners.resize(e->last_T);
+    gp_status s;
+    if ((s = e->ctx->cuda(cudaMemcpyAsync(e->kinds.data(), e->d_kinds.p, (size_t)n * 4, cudaMemcpyDeviceToHost, e->ctx->stream), "D2H kinds"))) return s;
+    if ((s = e->ctx->cuda(cudaMemcpyAsync(e->winners.data(), e->d_win.p, (size_t)e->last_T * 4, cudaMemcpyDeviceToHost, e->ctx->stream), "D2H winners"))) return s;
+    if ((s = e->ctx->cuda(cudaStreamSynchronize(e->ctx->stream), "selection sync"))) return s;
+  }
   if (kinds) *kinds = e->kinds.data();
   if (winners) *winners = e->winners.data();
   if (n_tournaments) *n_tournaments = (int32_t)e->winners.size();
+  return GP_OK;
+}
+
+gp_status gp_engine_set_population(gp_engine* e, const gp_node* nodes, const int64_t* offsets,
+                                   int32_t n_programs, int64_t n_nodes, const float* fitness,
+                                   int32_t generation, gp_generation_stats* stats_out) {
+  if (!e || !nodes || !offsets || generation < 0) return GP_ERR_ARG;
+  gp_context* ctx = e->ctx;
+  cudaSetDevice(ctx->device);
+  const gp_config& c = e->cfg;
+  if (n_programs != c.population_size || n_nodes < n_programs)
+    return ctx->fail(GP_ERR_ARG, "set_population: %d programs (population_size %d), %lld nodes",
+                     n_programs, c.population_size, (long long)n_nodes);
+  const int n = n_programs;
+  gp_status s;
+  gp_generation_stats st{};
+  const double t0 = now_s();
+  if (e->dev_mut && !is_host_pointer(nodes) && !is_host_pointer(offsets) && fitness &&
+      !is_host_pointer(fitness)) {
+    // device-resident population with known fitness: stream-ordered copies into the engine,
+    // statistics on the device (the programs are the caller's responsibility: a program deeper
+    // than the device scans makes the next generation fail with GP_ERR_PROGRAM)
+    if ((s = e->dev_buffers(n))) return s;
+    if ((s = ctx->grow(&e->d_nodes.p, &e->d_nodes.cap, (size_t)n_nodes * sizeof(gp_node), "d_nodes"))) return s;
+    if ((s = ctx->grow(&e->d_off.p, &e->d_off.cap, (size_t)(n + 1) * sizeof(int64_t), "d_off"))) return s;
+    if ((s = ctx->grow(&e->d_fit.p, &e->d_fit.cap, (size_t)n * sizeof(float), "d_fit"))) return s;
+    if ((s = ctx->grow(&e->d_status.p, &e->d_status.cap, (size_t)n * sizeof(uint32_t), "d_status"))) return s;
+    if ((s = ctx->cuda(cudaMemcpyAsync(e->d_nodes.p, nodes, (size_t)n_nodes * sizeof(gp_node), cudaMemcpyDeviceToDevice, ctx->stream), "D2D nodes"))) return s;
+    if ((s = ctx->cuda(cudaMemcpyAsync(e->d_off.p, offsets, (size_t)(n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream), "D2D offsets"))) return s;
+    if ((s = ctx->cuda(cudaMemcpyAsync(e->d_fit.p, fitness, (size_t)n * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream), "D2D fitness"))) return s;
+    e->n_nodes = n_nodes;
+    e->generation = generation;
+    e->host_view_valid = false;
+    e->pop.clear();
+    if ((s = e->dev_stats(n))) return s;
+    e->fill_stats_dev(&st);
+  } else {
+    // host copy, validated (prefix, depth <= capacity - 1), then the host upload path
+    std::vector<int64_t> off(n + 1);
+    std::vector<gp_node> nd((size_t)n_nodes);
+    if ((s = ctx->cuda(cudaMemcpy(off.data(), offsets, (size_t)(n + 1) * 8, cudaMemcpyDefault), "offsets"))) return s;
+    if ((s = ctx->cuda(cudaMemcpy(nd.data(), nodes, (size_t)n_nodes * sizeof(gp_node), cudaMemcpyDefault), "nodes"))) return s;
+    if (off[0] != 0 || off[n] != n_nodes) return ctx->fail(GP_ERR_ARG, "set_population: offsets");
+    std::vector<Prog> pop(n);
+    for (int i = 0; i < n; ++i) {
+      if (off[i + 1] <= off[i]) return ctx->fail(GP_ERR_ARG, "set_population: empty program %d", i);
+      Prog p(nd.begin() + off[i], nd.begin() + off[i + 1]);
+      int64_t needed = 1;
+      for (const gp_node& x : p) {
+        if (needed == 0 || arity(x.op) < 0) { needed = -1; break; }
+        needed += arity(x.op) - 1;
+      }
+      if (needed != 0) return ctx->fail(GP_ERR_ARG, "set_population: program %d is not a valid prefix list", i);
+      if (depth_of(p) > c.stack_capacity - 1) return ctx->fail(GP_ERR_ARG, "set_population: program %d too deep", i);
+      pop[i] = std::move(p);
+    }
+    e->pop.swap(pop);
+    e->generation = generation;
+    if ((s = e->evaluate(&st, fitness))) return s;
+    e->fill_stats(&st);
+  }
+  st.t_total_s = now_s() - t0;
+  if (stats_out) *stats_out = st;
   return GP_OK;
 }
 

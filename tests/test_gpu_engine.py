@@ -3,6 +3,8 @@
 Teacher forcing: each generation the oracle selects and mutates from the SAME fp32 fitness the GPU
 produced, so kinds, tournament winners and children must be bit-identical; the GPU fitness of the
 children is checked against the oracle's evaluation within the tolerance model."""
+import math
+
 import numpy as np
 import pytest
 
@@ -158,4 +160,89 @@ def test_full_size_wide_configs_sampled(gp, ctx, orc, cfg):
     sub_off[1:] = np.cumsum([lens[p] for p in sample])
     ref, sens, flags = orc.population_fitness(sub_nodes, sub_off, X, y, None, c["metric"])
     check_fitness(fit[sample], ref, sens, flags, c["metric"], max_excluded=1.0, max_ill=1.0)
+    e.close()
+
+
+# ---- GPU-side mutation ------------------------------------------------------------------
+@pytest.mark.parametrize("kw", [
+    dict(metric="mse"),
+    dict(metric="pearson"),
+    dict(metric="mae", p_crossover=0.2, p_subtree=0.3, p_hoist=0.2, p_point=0.25,
+         p_point_replace=0.3, function_set=list(range(2, 26)), stack_capacity=7,
+         init_depth_min=2, init_depth_max=6),
+    dict(metric="rmse", init_depth_min=2, init_depth_max=8, p_subtree=0.4, p_crossover=0.4,
+         p_hoist=0.1, p_point=0.05, const_lo=-5.0, const_hi=3.0),
+])
+def test_device_mutation_matches_host_mutation(gp, ctx, kw):
+    """The device path (mutate.cu) and the host path (engine.cpp) of gp_generation produce
+    bit-identical populations, selections and statistics over 8 generations -- crossover with
+    re-hoisting (small stack_capacity), subtree mutation with generated donors (init depth up to
+    8), hoist, point mutation over the whole catalog, reproduction."""
+    X, y = synth.pagie_grid(24)
+    X5 = np.ascontiguousarray(np.concatenate([X, X[::-1] * 0.5, X[:1] + 1.0]))  # 5 features
+    Xd, yd = dev(X5), dev(y)
+    engines = [gp.Engine(ctx, Xd, yd, population_size=300, seed=77, device_mutation=dm, **kw)
+               for dm in (1, 0)]
+    stats = [e.init_population() for e in engines]
+    keys = ("total_nodes", "best_index", "best_len", "best_depth", "max_stack_need",
+            "const_nodes", "const_programs", "op_count", "n_tournaments", "generation")
+    for g in range(8):
+        stats = [e.generation() for e in engines]
+        (n0, o0, f0), (n1, o1, f1) = engines[0].population(), engines[1].population()
+        assert np.array_equal(o0, o1) and np.array_equal(n0, n1), f"generation {g + 1}"
+        assert np.array_equal(f0, f1)
+        k0, w0 = engines[0].last_selection()
+        k1, w1 = engines[1].last_selection()
+        assert np.array_equal(k0, k1) and np.array_equal(w0, w1)
+        for k in keys:
+            assert stats[0][k] == stats[1][k], (g, k, stats[0][k], stats[1][k])
+        assert stats[0]["best_raw"] == stats[1]["best_raw"] or (
+            math.isnan(stats[0]["best_raw"]) and math.isnan(stats[1]["best_raw"]))
+        assert abs(stats[0]["mean_raw"] - stats[1]["mean_raw"]) <= 1e-9 * abs(stats[1]["mean_raw"])
+    for e in engines:
+        e.close()
+
+
+def test_device_mutation_depth_bound(gp, ctx, orc):
+    """Hoisted crossover keeps every child within depth stack_capacity - 1 on the device
+    path; the oracle's depth is the judge."""
+    X, y = synth.pagie_grid(16)
+    e = gp.Engine(ctx, dev(X), dev(y), population_size=400, seed=3, stack_capacity=5,
+                  init_depth_min=2, init_depth_max=4, p_crossover=0.9, p_subtree=0.1,
+                  p_hoist=0.0, p_point=0.0)
+    e.init_population()
+    for _ in range(6):
+        e.generation()
+        nodes, off, _ = e.population()
+        for p in range(len(off) - 1):
+            prog = nodes[off[p]:off[p + 1]]
+            assert orc.validate(prog) == 0 and orc.depth(prog) <= 4
+
+
+def test_set_population_and_reset(gp, ctx, orc):
+    """gp_engine_set_population: a host population is validated and evaluated (fitness == the
+    oracle's); re-seeding the device population with its fitness and generation reproduces the
+    same next generation (what bench.py does every step)."""
+    X, y = synth.pagie_grid(32)
+    Xd, yd = dev(X), dev(y)
+    e = gp.Engine(ctx, Xd, yd, population_size=200, metric="mse", seed=9)
+    nodes, off = synth.random_population(200, seed=4, depth=(1, 5))
+    st = e.set_population(nodes, off)
+    n2, o2, f2 = e.population()
+    assert np.array_equal(n2, nodes) and np.array_equal(o2, off)
+    ref, sens, flags = orc.population_fitness(nodes, off, X, y, None, "mse")
+    check_fitness(f2, ref, sens, flags, "mse", label="set_population")
+    assert st["total_nodes"] == len(nodes)
+    dn, do, df = e.population_device()
+    a = e.generation()
+    pa = e.population()
+    e.set_population(dn, do, df, generation=0)
+    b = e.generation()
+    pb = e.population()
+    assert all(np.array_equal(u, v) for u, v in zip(pa, pb))
+    assert a["total_nodes"] == b["total_nodes"] and a["best_index"] == b["best_index"]
+    bad = nodes.copy()
+    bad[0] = (99, 0)                                # not an opcode
+    with pytest.raises(gp.GPError):
+        e.set_population(bad, off)
     e.close()
