@@ -454,53 +454,46 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
   }
 }
 
-template <bool P, bool XS>
-static cudaError_t launch_t(const EvalArgs& a, int n_ctas, size_t smem, cudaStream_t s) {
+// ---- exports of this translation unit: ONE (PREDICT, XSMEM) instantiation ------------------------
+// build.py generates one translation unit per (shape, PREDICT, XSMEM) (GP_KP, GP_KXS) so the
+// heavy dispatch switch of each kernel compiles in parallel; eval_registry.cpp assembles the
+// EvalVariant of each shape from these functions.
+#if !defined(GP_KP) || !defined(GP_KXS)
+#error "define GP_KP and GP_KXS (generated translation units, build.py)"
+#endif
+#define GP_KTAG GP_CAT(GP_KP, GP_KXS)
+
+cudaError_t GP_CAT(launch_k, GP_KTAG)(const EvalArgs& a, int n_ctas, size_t smem, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(eval_kernel<P, XS>,
+    cudaError_t e = cudaFuncSetAttribute(eval_kernel<GP_KP, GP_KXS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  eval_kernel<P, XS><<<n_ctas, NT, smem, s>>>(a);
+  eval_kernel<GP_KP, GP_KXS><<<n_ctas, NT, smem, s>>>(a);
   return cudaGetLastError();
 }
 
-static cudaError_t launch(const EvalArgs& a, bool predict, bool xsmem, int n_ctas, size_t smem,
-                          cudaStream_t s) {
-#ifdef GP_GLOBAL_X_ONLY
-  if (xsmem) return cudaErrorInvalidValue;
-  return predict ? launch_t<true, false>(a, n_ctas, smem, s) : launch_t<false, false>(a, n_ctas, smem, s);
-#else
-  if (predict) return xsmem ? launch_t<true, true>(a, n_ctas, smem, s) : launch_t<true, false>(a, n_ctas, smem, s);
-  return xsmem ? launch_t<false, true>(a, n_ctas, smem, s) : launch_t<false, false>(a, n_ctas, smem, s);
-#endif
-}
-
-template <bool P, bool XS>
-static int occ_t(size_t smem) {
+// resident CTAs per SM for a dynamic shared-memory size (memoised: the size rarely changes)
+int GP_CAT(occ_k, GP_KTAG)(size_t smem) {
+  thread_local size_t last_smem = ~(size_t)0;
+  thread_local int last_n = 0;
+  if (smem == last_smem) return last_n;
   int n = 0;
-  cudaFuncSetAttribute(eval_kernel<P, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, eval_kernel<P, XS>, NT, smem);
+  cudaFuncSetAttribute(eval_kernel<GP_KP, GP_KXS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kMaxDynSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, eval_kernel<GP_KP, GP_KXS>, NT, smem);
+  last_smem = smem;
+  last_n = n;
   return n;
 }
-static int occupancy(bool predict, bool xsmem, size_t smem) {
-#ifdef GP_GLOBAL_X_ONLY
-  if (xsmem) return 0;
-  return predict ? occ_t<true, false>(smem) : occ_t<false, false>(smem);
-#else
-  if (predict) return xsmem ? occ_t<true, true>(smem) : occ_t<true, false>(smem);
-  return xsmem ? occ_t<false, true>(smem) : occ_t<false, false>(smem);
+
+#if GP_KP == 0 && ((defined(GP_GLOBAL_X_ONLY) && GP_KXS == 0) || (!defined(GP_GLOBAL_X_ONLY) && GP_KXS == 1))
+// the shape's static description (exported once per shape)
+EvalShape shape_info() { return EvalShape{STACK, R, SUB, NT}; }
+size_t acc_bytes(int G, int S) { return smem_acc_bytes(G, S); }
 #endif
-}
 
 }  // namespace GP_NS
-
-const EvalVariant& GP_CAT(eval_variant_, GP_NS)() {
-  static const EvalVariant v = {EvalShape{GP_NS::STACK, GP_NS::R, GP_NS::SUB, GP_NS::NT},
-                                &GP_NS::launch, &GP_NS::occupancy, &GP_NS::smem_acc_bytes};
-  return v;
-}
-
 }  // namespace gpb

@@ -4,4 +4,4 @@
 #define GP_SUB 4
 #define GP_NT 128
 #define GP_MINB 4
-#include "eval_impl.cuh"
+

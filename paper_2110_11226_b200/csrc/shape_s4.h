@@ -5,4 +5,4 @@
 #define GP_SUB 1
 #define GP_NT 128
 #define GP_MINB 4
-#include "eval_impl.cuh"
+

@@ -8,4 +8,4 @@
 #define GP_MINB_GLOBAL 3
 #define GP_RED_ROWS 8
 #define GP_GLOBAL_X_ONLY 1
-#include "eval_impl.cuh"
+
