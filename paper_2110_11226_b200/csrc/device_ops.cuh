@@ -32,6 +32,35 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
+// Reciprocal on the FMA pipe instead of MUFU.RCP (GP_RCP_FMA = 1; default 0 = MUFU.RCP). A third
+// of the MUFU work of the paper's function set is the reciprocal of div and tan and the FMA pipe
+// has 8x the XU's throughput, but the r02 A/B (profiles/ab_r02_rcp.log) measured C3 134 -> 242 ms
+// per step and C5 / C4 slower too: the evaluator is bound by issue and latency around the SFU, and
+// 12 more instructions per row pair (plus register pressure: spills at the 128-register budget)
+// cost more than the XU time they free. Kept as a documented option. Seed: the magic-constant estimate
+// of 1/|b| (5 % relative error), then three Newton steps r += r (1 - |b| r) -- <= 0.59 ulp over
+// every normal |b| (numpy emulation of the FFMA sequence over 2^-126..2^126), i.e. as accurate as
+// rcp.approx (the oracle's budget for div / inv is 3 u). |b| > 2^126
+// -> 0 (the flushed result); 0 -> inf; NaN propagates. Branch-free. The _x2 form runs two rows
+// through FFMA2 with the same roundings (bit-identical to two scalar calls).
+#ifndef GP_RCP_FMA
+#define GP_RCP_FMA 0
+#endif
+constexpr int kRcpMagic = 0x7EF311C7;
+constexpr float kRcpHuge = 8.50705917e37f;   // 2^126
+__device__ __forceinline__ float rcp_fast(float b) {
+#if GP_RCP_FMA
+  const float ab = fabsf(b);
+  float r = __int_as_float(kRcpMagic - __float_as_int(ab)), e;
+  e = fmaf(-ab, r, 1.0f); r = fmaf(r, e, r);
+  e = fmaf(-ab, r, 1.0f); r = fmaf(r, e, r);
+  e = fmaf(-ab, r, 1.0f); r = fmaf(r, e, r);
+  return copysignf(ab > kRcpHuge ? 0.0f : r, b);
+#else
+  return rcp_approx(b);
+#endif
+}
+
 // a = first operand (first popped), b = second operand.
 __device__ __forceinline__ float ex2_approx(float x) {
   float r;
@@ -103,7 +132,7 @@ __device__ __forceinline__ float apply2(float a, float b) {
   if constexpr (OP == GP_OP_ADD) return a + b;
   else if constexpr (OP == GP_OP_SUB) return a - b;
   else if constexpr (OP == GP_OP_MUL) return a * b;
-  else if constexpr (OP == GP_OP_DIV) { const float q = a * rcp_approx(b); return fabsf(b) < kProt ? 1.0f : q; }
+  else if constexpr (OP == GP_OP_DIV) { const float q = a * rcp_fast(b); return fabsf(b) < kProt ? 1.0f : q; }
   else if constexpr (OP == GP_OP_MIN) return fminf(a, b);
   else if constexpr (OP == GP_OP_MAX) return fmaxf(a, b);
   else {  // GP_OP_POW: |a|^b = 2^(b * log2|a|), clamped; 0^b and b == 0 by selects
@@ -117,13 +146,13 @@ template <int OP>
 __device__ __forceinline__ float apply1(float a) {
   if constexpr (OP == GP_OP_SIN) return __sinf(a);
   else if constexpr (OP == GP_OP_COS) return __cosf(a);
-  else if constexpr (OP == GP_OP_TAN) return __sinf(a) * rcp_approx(__cosf(a));
+  else if constexpr (OP == GP_OP_TAN) return __sinf(a) * rcp_fast(__cosf(a));
   else if constexpr (OP == GP_OP_ABS) return fabsf(a);
   else if constexpr (OP == GP_OP_NEG) return -a;
   else if constexpr (OP == GP_OP_SQRT) return sqrt_approx(fabsf(a));
   else if constexpr (OP == GP_OP_LOG) { const float l = __logf(fabsf(a)); return fabsf(a) < kProt ? 0.0f : l; }
   else if constexpr (OP == GP_OP_EXP) return fminf(__expf(a), kBig);
-  else if constexpr (OP == GP_OP_INV) { const float r = rcp_approx(a); return fabsf(a) < kProt ? 1.0f : r; }
+  else if constexpr (OP == GP_OP_INV) { const float r = rcp_fast(a); return fabsf(a) < kProt ? 1.0f : r; }
   else if constexpr (OP == GP_OP_SQUARE) return a * a;
   else if constexpr (OP == GP_OP_CUBE) return a * a * a;
   else if constexpr (OP == GP_OP_TANH) return tanh_bf(a);
@@ -160,6 +189,26 @@ __device__ __forceinline__ void fma_x2(float& d0, float& d1, float a0, float a1,
 }
 #undef GPB_X2
 
+// rcp_fast on two rows (FFMA2), bit-identical to two rcp_fast calls
+__device__ __forceinline__ void rcp_fast_x2(float& r0, float& r1, float b0, float b1) {
+#if GP_RCP_FMA
+  const float a0 = fabsf(b0), a1 = fabsf(b1);
+  float x0 = __int_as_float(kRcpMagic - __float_as_int(a0));
+  float x1 = __int_as_float(kRcpMagic - __float_as_int(a1));
+  float e0, e1;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    fma_x2(e0, e1, -a0, -a1, x0, x1, 1.0f, 1.0f);
+    fma_x2(x0, x1, x0, x1, e0, e1, x0, x1);
+  }
+  r0 = copysignf(a0 > kRcpHuge ? 0.0f : x0, b0);
+  r1 = copysignf(a1 > kRcpHuge ? 0.0f : x1, b1);
+#else
+  r0 = rcp_approx(b0);
+  r1 = rcp_approx(b1);
+#endif
+}
+
 // apply2 on two rows: (d0, d1) = (a0 OP b0, a1 OP b1), bit-identical to two apply2 calls.
 template <int OP>
 __device__ __forceinline__ void apply2_x2(float& d0, float& d1, float a0, float a1, float b0,
@@ -168,8 +217,9 @@ __device__ __forceinline__ void apply2_x2(float& d0, float& d1, float a0, float 
   else if constexpr (OP == GP_OP_SUB) sub_x2(d0, d1, a0, a1, b0, b1);
   else if constexpr (OP == GP_OP_MUL) mul_x2(d0, d1, a0, a1, b0, b1);
   else if constexpr (OP == GP_OP_DIV) {
-    float q0, q1;
-    mul_x2(q0, q1, a0, a1, rcp_approx(b0), rcp_approx(b1));
+    float q0, q1, i0, i1;
+    rcp_fast_x2(i0, i1, b0, b1);
+    mul_x2(q0, q1, a0, a1, i0, i1);
     d0 = fabsf(b0) < kProt ? 1.0f : q0;
     d1 = fabsf(b1) < kProt ? 1.0f : q1;
   } else {
@@ -187,7 +237,14 @@ __device__ __forceinline__ void apply1_x2(float& d0, float& d1, float a0, float 
     mul_x2(s0, s1, a0, a1, a0, a1);
     mul_x2(d0, d1, s0, s1, a0, a1);
   } else if constexpr (OP == GP_OP_TAN) {
-    mul_x2(d0, d1, __sinf(a0), __sinf(a1), rcp_approx(__cosf(a0)), rcp_approx(__cosf(a1)));
+    float i0, i1;
+    rcp_fast_x2(i0, i1, __cosf(a0), __cosf(a1));
+    mul_x2(d0, d1, __sinf(a0), __sinf(a1), i0, i1);
+  } else if constexpr (OP == GP_OP_INV) {
+    float i0, i1;
+    rcp_fast_x2(i0, i1, a0, a1);
+    d0 = fabsf(a0) < kProt ? 1.0f : i0;
+    d1 = fabsf(a1) < kProt ? 1.0f : i1;
   } else {
     const float r0 = apply1<OP>(a0), r1 = apply1<OP>(a1);
     d0 = r0;

@@ -1,14 +1,14 @@
 // Evaluator variant for wide datasets (X columns read through L1/L2, no shared-memory X tile):
-// register stack of 4 slots, 8 rows per thread, 256-thread CTAs at an 80-register budget (3 CTAs
-// = 24 warps per SM). The L2 latency of the per-word variable loads needs more resident warps
-// than the shared-memory-X shape (128 threads x 16 rows, 16 warps) provides; measured on C5
-// (Year-shaped 1M x 90): SFU frac 0.35 -> 0.53 (DESIGN.md performance log).
+// register stack of 4 slots, 4 rows per thread, 512-thread CTAs at a 32-register budget (4 CTAs =
+// 64 warps per SM, full occupancy). The variable operands are L2 loads (a 2048-row tile of 28-90
+// columns does not fit shared memory), so the shape that hides their latency best wins: measured
+// on C5 / C4 (r02 A/B, tools/ab_libs.sh): 256 x 8 rows at 80 registers (24 warps) 0.31 / 0.39 SFU
+// frac of the step, 512 x 4 at 64 / 40 / 32 registers 0.39 / 0.44, 0.44 / 0.47, 0.46 / 0.50.
 #define GP_STACK 4
-#define GP_R 8
+#define GP_R 4
 #define GP_SUB 1
-#define GP_NT 256
-#define GP_MINB 3
-#define GP_MINB_GLOBAL 3
+#define GP_NT 512
+#define GP_MINB 4
+#define GP_MINB_GLOBAL 4
 #define GP_RED_ROWS 8
 #define GP_GLOBAL_X_ONLY 1
-
