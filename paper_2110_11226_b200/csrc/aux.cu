@@ -344,10 +344,17 @@ __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __res
   const int len = code_len[p];
   const uint4* src = code + code_off[p];
   uint4* dst = stream + pos[i];
+  const int caps[kNumVariants] = {4, 8, 12, 20};   // kVariantStack
+  const int vstack = caps[b];            // the variant's dispatch numbering (device_ops opv_rank)
   // the group's stream [gs, ge): words at window ends get kEndWin
   const int64_t gs = gstart[(int64_t)b * (n + 1) + j / G], ge = gstart[(int64_t)b * (n + 1) + j / G + 1];
   for (int pass = 0; pass < subs[b]; ++pass) {
-    for (int k = 0; k < len; ++k) *dst++ = src[k];
+    for (int k = 0; k < len; ++k) {
+      uint4 w = src[k];
+      const int opv = (int)w.x / kCaseStride, slot = (int)w.x - opv * kCaseStride;
+      w.x = (uint32_t)(opv_rank(opv) * vstack + slot);
+      *dst++ = w;
+    }
     const bool last = pass == subs[b] - 1;
     dst[-1].w = last ? (kEndProgram | ((uint32_t)(j % G) << 8))
                      : (kEndPass | ((uint32_t)(pass + 1) << 8));

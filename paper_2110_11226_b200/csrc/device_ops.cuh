@@ -306,4 +306,22 @@ enum { UV_S = 0, UV_V, UV_C };
 __host__ __device__ constexpr int opv_bin(int op, int v) { return OPV_BIN0 + (op - GP_OP_ADD) * 10 + v; }
 __host__ __device__ constexpr int opv_un(int op, int u) { return OPV_UN0 + (op - GP_OP_SIN) * 3 + u; }
 
+// Dispatch numbering of the evaluator (pack_kernel rewrites the stage kernel's case ids into it):
+// case = opv_rank(opv) * STACK + slot with the variant's own slot count (not kCaseStride), and
+// the paper's function set first -- push, add / sub / mul / div (all operand variants), sin / cos /
+// tan -- so the jump table the hot loop indexes is small and dense (s4: 204 hot entries in 816 B
+// instead of ~1 in 5 entries used over 9.8 KB): the ncu SASS profile of r02 put 9 % of all stall
+// samples on the jump-table constant load (profiles/ncu_eval_r02_c3gen0_base.md).
+__host__ __device__ constexpr int opv_rank(int opv) {
+  if (opv < OPV_BIN0) return opv;                                   // push var / const: 0, 1
+  if (opv < OPV_UN0) {
+    const int o = GP_OP_ADD + (opv - OPV_BIN0) / 10, v = (opv - OPV_BIN0) % 10;
+    return o <= GP_OP_DIV ? 2 + (o - GP_OP_ADD) * 10 + v            // 2 .. 41
+                          : 51 + (o - GP_OP_MIN) * 10 + v;          // 51 .. 80
+  }
+  const int o = GP_OP_SIN + (opv - OPV_UN0) / 3, u = (opv - OPV_UN0) % 3;
+  return o <= GP_OP_TAN ? 42 + (o - GP_OP_SIN) * 3 + u              // 42 .. 50
+                        : 81 + (o - GP_OP_ABS) * 3 + u;             // 81 .. 122
+}
+
 }  // namespace gpb

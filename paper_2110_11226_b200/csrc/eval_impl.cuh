@@ -64,6 +64,7 @@ static_assert(RR == 8 || RR == 16, "reduction block: 8 or 16 programs");
 static_assert(R % 4 == 0 && NT % 32 == 0, "R must be a multiple of 4");
 static_assert(TILE == kTile, "every variant shares the row tile");
 static_assert(STACK <= kCaseStride, "slot must fit the case stride");
+static_assert(opv_rank(OPV_COUNT - 1) < OPV_COUNT, "opv_rank is a permutation of 0..OPV_COUNT-1");
 
 // dynamic shared-memory opt-in: 227 KB per CTA minus the kernel's static shared memory
 constexpr int kMaxDynSmem = 220 * 1024;
@@ -79,7 +80,7 @@ __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
   return (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15) + RED_BYTES;
 }
 
-#define LBL(OPV, s) ((OPV) * kCaseStride + (s))
+#define LBL(OPV, s) (opv_rank(OPV) * STACK + (s))   // pack_kernel's numbering
 
 // -- dispatch cases -------------------------------------------------------------------------------
 // Cases work on 4-row chunks (one LDS.128 of a variable per chunk), so a fused variable operand
