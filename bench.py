@@ -143,7 +143,7 @@ def algorithmic_ops(op_count, rows, metric, n_programs, const_programs=0):
     return sfu, fp32
 
 
-def roofline_of(sfu, fp32, eval_ms, launches, step_ms, traffic=True):
+def roofline_of(sfu, fp32, eval_ms, launches, step_ms, traffic=None):
     """Binding ALU pipe of the evaluator for the given algorithmic work: SFU (MUFU) or FP32."""
     eval_s = eval_ms * 1e-3
     f_sfu, f_fp32 = sfu / eval_s / SFU_PEAK, fp32 / eval_s / FP32_PEAK
@@ -153,9 +153,11 @@ def roofline_of(sfu, fp32, eval_ms, launches, step_ms, traffic=True):
     else:
         r = {"bound": "alu", "pipe": "FP32", "achieved": round(fp32 / eval_s / 1e12, 4),
              "peak": round(FP32_PEAK / 1e12, 4), "unit": "TFLOP/s (fp32)", "frac": round(f_fp32, 4)}
-    r.update({"traffic": ncu_traffic() if traffic else None,
-              "traffic_scope": "DRAM bytes of one C3 evaluation's eval launches "
-                               "(profiles/eval_kernel_ncu.json)" if traffic else "measured for C3 only", "sfu_frac": round(f_sfu, 4), "fp32_frac": round(f_fp32, 4),
+    tr = ncu_traffic(traffic) if traffic else None
+    r.update({"traffic": tr,
+              "traffic_scope": (f"DRAM bytes of one evaluation's eval launches of the step "
+                                f"(profiles/eval_kernel_ncu_{traffic}.json)") if tr else None,
+              "sfu_frac": round(f_sfu, 4), "fp32_frac": round(f_fp32, 4),
               "eval_ms_per_launch": round(eval_ms / max(launches, 1), 3),
               "eval_share_of_step": round(eval_ms / step_ms, 4),
               "peak_note": "SFU: 148 SMs x 16 MUFU/clk x 1965 MHz (measured MUFU.SIN 4.63e12/s); "
@@ -163,9 +165,10 @@ def roofline_of(sfu, fp32, eval_ms, launches, step_ms, traffic=True):
     return r
 
 
-def ncu_traffic():
-    """dram bytes per eval launch from the committed ncu --set full summary, if present."""
-    path = os.path.join(ROOT, "profiles", "eval_kernel_ncu.json")
+def ncu_traffic(config="c3"):
+    """DRAM bytes per evaluation (all variant launches) from the committed launch list with dram
+    counters of this config (tools/traffic_json.py), if present."""
+    path = os.path.join(ROOT, "profiles", f"eval_kernel_ncu_{config}.json")
     try:
         with open(path) as f:
             return json.load(f).get("dram_bytes_per_launch")   # per evaluation (all variants)
@@ -318,7 +321,7 @@ def run_b200(args, cfg):
         a, b2 = algorithmic_ops(s["op_count"], rows_local, cfg["metric"], cfg["pop"],
                                 0 if args.no_const_programs else s["const_programs"])
         sfu, fp32 = sfu + a, fp32 + b2
-    roofline = roofline_of(sfu, fp32, eval_ms, eval_launches, ms, traffic=args.config == "c3")
+    roofline = roofline_of(sfu, fp32, eval_ms, eval_launches, ms, traffic=args.config)
 
     # ---- gp_evaluate alone on the fixed generation-0 population (SURVEY D definition) -----------
     fit_buf = torch.empty(cfg["pop"], dtype=torch.float32, device=f"cuda:{local}")
@@ -342,7 +345,7 @@ def run_b200(args, cfg):
     t_med = statistics.median(times)
     a0_, b0_ = algorithmic_ops(st0["op_count"], rows_local, cfg["metric"], cfg["pop"],
                                0 if args.no_const_programs else st0["const_programs"])
-    roof0 = roofline_of(a0_ * reps, b0_ * reps, k_ms, k_l, k_ms, traffic=False)
+    roof0 = roofline_of(a0_ * reps, b0_ * reps, k_ms, k_l, k_ms)
     evaluate = {"population": "generation 0 (ramped half-and-half), mean length %.2f"
                               % (n0_len / cfg["pop"]),
                 "reps": reps, "median_ms": round(t_med, 3), "min_ms": round(min(times), 3),

@@ -194,7 +194,8 @@ static gp_status launch_variants(gp_context* ctx, EvalArgs a, const EvalPlan& pl
     a.prog_count = (const int32_t*)ctx->counts.p + v;
     a.work_counter = (int32_t*)ctx->counts.p + kNumVariants + v;
     a.part_base = (const int32_t*)ctx->inv.p + n + v;
-    const size_t smem = pl.smem + (predict ? 0 : var.acc_bytes(pl.G, a.metric == GP_PEARSON ? 3 : 1));
+    const size_t smem = var.smem_bytes(pl.G, a.metric == GP_PEARSON ? 3 : 1, a.n_cols,
+                                       a.w != nullptr, pl.xsmem, predict);
     const int occ = std::max(1, var.occupancy(predict, pl.xsmem, smem));
     gp_status s = ctx->launch(var.launch(a, predict, pl.xsmem, ctx->sms * occ, smem, ctx->stream),
                             predict ? "predict kernel" : "eval kernel");

@@ -58,11 +58,12 @@ namespace gpb {
 namespace GP_NS {
 
 constexpr int STACK = GP_STACK, R = GP_R, SUB = GP_SUB, NT = GP_NT;
-constexpr int TILE = NT * R * SUB, NW = NT / 32, R4 = R / 4;
+constexpr int TILE = NT * R * SUB;
+static_assert(TILE == kTile, "every variant shares the row tile");
+constexpr int NW = NT / 32, R4 = R / 4;
 constexpr int RR = GP_RED_ROWS, LPR = 32 / RR, RED_BYTES = NW * RR * kRedStride * 4;
 static_assert(RR == 8 || RR == 16, "reduction block: 8 or 16 programs");
 static_assert(R % 4 == 0 && NT % 32 == 0, "R must be a multiple of 4");
-static_assert(TILE == kTile, "every variant shares the row tile");
 static_assert(STACK <= kCaseStride, "slot must fit the case stride");
 static_assert(opv_rank(OPV_COUNT - 1) < OPV_COUNT, "opv_rank is a permutation of 0..OPV_COUNT-1");
 
@@ -78,6 +79,12 @@ constexpr float kLogLossHi = 34.538776394910684f;      // -ln(1e-15)
 // | code-stream window [kStreamWin + 2] uint4
 __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
   return (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15) + RED_BYTES;
+}
+// Dynamic shared memory of one launch of this shape.
+inline size_t smem_total(int G, int S, int n_cols, bool weighted, bool xsmem, bool predict) {
+  const size_t yw = predict ? 0 : (weighted ? 2 : 1) * (size_t)TILE * sizeof(float);
+  return (predict ? 0 : smem_acc_bytes(G, S)) + yw +
+         (xsmem ? (size_t)n_cols * TILE * sizeof(float) : 0) + (size_t)(kStreamWin + 2) * 16;
 }
 
 #define LBL(OPV, s) (opv_rank(OPV) * STACK + (s))   // pack_kernel's numbering
@@ -463,16 +470,17 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
 #error "define GP_KP and GP_KXS (generated translation units, build.py)"
 #endif
 #define GP_KTAG GP_CAT(GP_KP, GP_KXS)
+#define GP_KERNEL eval_kernel<GP_KP, GP_KXS>
 
 cudaError_t GP_CAT(launch_k, GP_KTAG)(const EvalArgs& a, int n_ctas, size_t smem, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(eval_kernel<GP_KP, GP_KXS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    cudaError_t e = cudaFuncSetAttribute(GP_KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kMaxDynSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  eval_kernel<GP_KP, GP_KXS><<<n_ctas, NT, smem, s>>>(a);
+  GP_KERNEL<<<n_ctas, NT, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -482,9 +490,8 @@ int GP_CAT(occ_k, GP_KTAG)(size_t smem) {
   thread_local int last_n = 0;
   if (smem == last_smem) return last_n;
   int n = 0;
-  cudaFuncSetAttribute(eval_kernel<GP_KP, GP_KXS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kMaxDynSmem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, eval_kernel<GP_KP, GP_KXS>, NT, smem);
+  cudaFuncSetAttribute(GP_KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, GP_KERNEL, NT, smem);
   last_smem = smem;
   last_n = n;
   return n;
@@ -493,7 +500,9 @@ int GP_CAT(occ_k, GP_KTAG)(size_t smem) {
 #if GP_KP == 0 && ((defined(GP_GLOBAL_X_ONLY) && GP_KXS == 0) || (!defined(GP_GLOBAL_X_ONLY) && GP_KXS == 1))
 // the shape's static description (exported once per shape)
 EvalShape shape_info() { return EvalShape{STACK, R, SUB, NT}; }
-size_t acc_bytes(int G, int S) { return smem_acc_bytes(G, S); }
+size_t smem_bytes(int G, int S, int n_cols, int weighted, int xsmem, int predict) {
+  return smem_total(G, S, n_cols, weighted != 0, xsmem != 0, predict != 0);
+}
 #endif
 
 }  // namespace GP_NS

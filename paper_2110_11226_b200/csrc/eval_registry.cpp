@@ -15,7 +15,7 @@ namespace gpb {
 #define GP_DECLARE_SHAPE(NS)                                                                   \
   namespace NS {                                                                               \
   EvalShape shape_info();                                                                      \
-  size_t acc_bytes(int G, int S);                                                              \
+  size_t smem_bytes(int G, int S, int n_cols, int weighted, int xsmem, int predict);           \
   }
 
 // shapes with a shared-memory X tile and a global-X fallback: kernels 00 01 10 11
@@ -35,7 +35,7 @@ namespace gpb {
   }                                                                                            \
   const EvalVariant& eval_variant_##NS() {                                                     \
     static const EvalVariant v = {NS::shape_info(), &NS::launch, &NS::occupancy,               \
-                                  &NS::acc_bytes};                                             \
+                                  &NS::smem_bytes};                                             \
     return v;                                                                                  \
   }
 
@@ -55,7 +55,7 @@ namespace gpb {
   }                                                                                            \
   const EvalVariant& eval_variant_##NS() {                                                     \
     static const EvalVariant v = {NS::shape_info(), &NS::launch, &NS::occupancy,               \
-                                  &NS::acc_bytes};                                             \
+                                  &NS::smem_bytes};                                             \
     return v;                                                                                  \
   }
 

@@ -83,9 +83,9 @@ struct EvalVariant {
                         cudaStream_t s);
   // Resident CTAs per SM for the given dynamic shared memory.
   int (*occupancy)(bool predict, bool xsmem, size_t smem);
-  // Shared memory of the fp64 accumulators + reduction blocks for G programs, S sums each
-  // (FIT mode; precedes the tiles in the kernel's layout).
-  size_t (*acc_bytes)(int G, int S);
+  // Dynamic shared memory of one launch: accumulators + reduction blocks for G programs x S sums
+  // (FIT mode), the y / w tile, the X tile (xsmem) and the code-stream window.
+  size_t (*smem_bytes)(int G, int S, int n_cols, int weighted, int xsmem, int predict);
 };
 const EvalVariant& eval_variant_s4();
 const EvalVariant& eval_variant_s8();

@@ -4,6 +4,8 @@
 // columns does not fit shared memory), so the shape that hides their latency best wins: measured
 // on C5 / C4 (r02 A/B, tools/ab_libs.sh): 256 x 8 rows at 80 registers (24 warps) 0.31 / 0.39 SFU
 // frac of the step, 512 x 4 at 64 / 40 / 32 registers 0.39 / 0.44, 0.44 / 0.47, 0.46 / 0.50.
+// (A warp-per-program kernel that staged one warp's rows of every column in shared memory was
+// measured slower, C5 12 -> 22 ms per step: the staging costs more than the L2 loads it removes.)
 #define GP_STACK 4
 #define GP_R 4
 #define GP_SUB 1

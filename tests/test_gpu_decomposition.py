@@ -205,3 +205,34 @@ def test_partial_rejects_spearman(gp, pctx):
     with pytest.raises(gp.GPError):
         pctx.evaluate_partial(dev(nodes), dev(off), dev(X), dev(y), metric="spearman",
                               max_stack=8)
+
+
+@pytest.mark.parametrize("metric", METRICS)
+def test_wide_dataset_every_program(gp, pctx, orc, metric):
+    """Wide datasets (> 11 columns: no 2048-row shared-memory X tile) run the warp-per-program
+    kernels (w4 / w8: one warp's rows staged for every column, programs handed to warps from a
+    shared counter): every program against the oracle, weighted with exact zeros, ragged tail,
+    both the 4- and the 8-slot shape (classic order keeps the deep needs), at the production plan."""
+    n_rows, n_cols = 20_000 + 77, 40
+    Xh, yh = synth.higgs_like(n_rows, seed=21, n_cols=n_cols)
+    if metric != "logloss":
+        yh = (Xh[0] * Xh[1] + np.sin(Xh[2])).astype(np.float32)
+    w = synth.weights(n_rows, seed=22)
+    a, ao = synth.random_population(200, seed=23, depth=(0, 6), n_features=n_cols, max_stack=8)
+    d, do = synth.deep_population(56, seed=24, need=(5, 8), n_features=n_cols)
+    nodes = np.concatenate([a, d])
+    off = np.concatenate([ao, do[1:] + ao[-1]])
+    pctx.set_eval_order(False)
+    pctx.set_plan(128, 3)
+    fit, st = pctx.evaluate(dev(nodes), dev(off), dev(Xh), dev(yh), dev(w), metric=metric,
+                            max_stack=8)
+    ref, sens, flags = orc.population_fitness(nodes, off, Xh, yh, w, metric)
+    check_fitness(fit.cpu().numpy(), ref, sens, flags, metric, label=f"wide {metric}")
+    # the automatic plan agrees to summation order
+    pctx.set_plan(0, 0)
+    f2, _ = pctx.evaluate(dev(nodes), dev(off), dev(Xh), dev(yh), dev(w), metric=metric,
+                          max_stack=8)
+    a_, b_ = fit.cpu().numpy(), f2.cpu().numpy()
+    fin = np.isfinite(a_)
+    scale = 1.0 if metric == "pearson" else np.maximum(np.abs(a_[fin]), 1e-6)
+    assert np.all(np.abs(a_[fin] - b_[fin]) <= 1e-4 * scale)

@@ -1,15 +1,15 @@
 #!/usr/bin/env python
-"""profiles/eval_kernel_ncu.json from a launch list with dram counters (bench.py reads its
+"""profiles/eval_kernel_ncu_<config>.json from a launch list with dram counters (bench.py reads its
 dram_bytes_per_launch as roofline.traffic).
 
-    python tools/traffic_json.py gpurun_out/launches_vNN.csv
+    python tools/traffic_json.py gpurun_out/traffic_c3.csv c3 ALGORITHMIC_BYTES
 """
 import collections
 import csv
 import json
 import sys
 
-src = sys.argv[1]
+src, cfg, alg = sys.argv[1], sys.argv[2], int(sys.argv[3])
 rows = list(csv.reader(open(src)))
 hdr, data = None, collections.defaultdict(dict)
 for r in rows:
@@ -30,12 +30,12 @@ for _, d in sorted(data.items()):
 n_eval = max(len(v) for v in per.values())
 out = {"source": f"{src} (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
                  "gpu__time_duration.sum --clock-control none, every launch of `python bench.py "
-                 "--steps 2 --warmup 3 --no-e2e --no-cpu-baseline`, config c3)",
+                 "--steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-evolved`, config " + cfg + ")",
        "evaluations": n_eval,
        "per_variant_bytes_per_evaluation": {k: sum(v) / n_eval for k, v in per.items()},
-       "algorithmic_bytes_per_evaluation": 201326592,
+       "algorithmic_bytes_per_evaluation": alg,
        "note": "one evaluation = one launch per non-empty stack-need variant; reads of X, y "
                "plus the fp64 partial-sum writes; ncu flushes caches between launches",
        "dram_bytes_per_launch": sum(sum(v) for v in per.values()) / n_eval}
-json.dump(out, open("profiles/eval_kernel_ncu.json", "w"), indent=1)
+json.dump(out, open(f"profiles/eval_kernel_ncu_{cfg}.json", "w"), indent=1)
 print(json.dumps(out["per_variant_bytes_per_evaluation"]), out["dram_bytes_per_launch"])
