@@ -634,6 +634,51 @@ struct gp_engine {
     return GP_OK;
   }
 
+  // Generation 0 on the GPU (program generation): ramped half-and-half from the same
+  // Philox streams as the host path, evaluated, statistics read once. [sync]
+  gp_status device_init(gp_generation_stats* st_out) {
+    const int n = cfg.population_size;
+    const double t0 = now_s();
+    gp_status s;
+    if ((s = dev_buffers(n))) return s;
+    if ((s = ctx->grow(&d_off.p, &d_off.cap, (size_t)(n + 1) * sizeof(int64_t), "d_off"))) return s;
+    if ((s = ctx->grow(&d_fit.p, &d_fit.cap, (size_t)n * sizeof(float), "d_fit"))) return s;
+    if ((s = ctx->grow(&d_status.p, &d_status.cap, (size_t)n * sizeof(uint32_t), "d_status"))) return s;
+    const MutConfig mc = mut_config();
+    cudaStream_t str = ctx->stream;
+    cudaEventRecord(ev[0], str);
+    if ((s = ctx->launch(launch_init_lengths(n, mc, (int32_t*)d_len.p, (int64_t*)d_off.p, str), "init lengths"))) return s;
+    ctx->kernel_launches += 1;
+    int64_t total = 0;
+    if ((s = ctx->cuda(cudaMemcpyAsync(&total, (int64_t*)d_off.p + n, 8, cudaMemcpyDeviceToHost, str), "D2H total"))) return s;
+    if ((s = ctx->cuda(cudaStreamSynchronize(str), "init sync"))) return s;
+    if ((s = ctx->grow(&d_nodes.p, &d_nodes.cap, (size_t)std::max<int64_t>(total, 1) * sizeof(gp_node), "d_nodes"))) return s;
+    if ((s = ctx->launch(launch_init_emit(n, mc, (const int64_t*)d_off.p, (gp_node*)d_nodes.p, str), "init emit"))) return s;
+    cudaEventRecord(ev[1], str);
+    n_nodes = total;
+    generation = 0;
+    host_view_valid = false;
+    pop.clear();
+    kinds.clear();
+    winners.clear();
+    last_T = 0;
+    if ((s = gp_evaluate(ctx, (const gp_node*)d_nodes.p, (const int64_t*)d_off.p, n, total,
+                         std::min(cfg.stack_capacity, GP_MAX_STACK), X, ldx, y, w, n_rows, n_cols,
+                         (gp_metric)cfg.metric, (float*)d_fit.p, (uint32_t*)d_status.p))) return s;
+    cudaEventRecord(ev[2], str);
+    if ((s = dev_stats(n))) return s;
+    gp_generation_stats st{};
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    st.t_mutate_s = 1e-3 * a;                     // program generation
+    st.t_eval_s = 1e-3 * b;
+    fill_stats_dev(&st);
+    st.t_total_s = now_s() - t0;
+    if (st_out) *st_out = st;
+    return GP_OK;
+  }
+
   void fill_stats(gp_generation_stats* st) {
     const int n = (int)pop.size();
     int best = -1;
@@ -748,6 +793,7 @@ gp_status gp_engine_init_population(gp_engine* e, gp_generation_stats* stats_out
   const double t0 = now_s();
   const gp_config& c = e->cfg;
   const int n = c.population_size;
+  if (e->dev_mut) return e->device_init(stats_out);
   e->pop.assign(n, Prog());
   parallel_for(e->pool.get(), n, [&](int i) {
     Rng r(c.seed, (uint32_t)i, 0u, 3u);

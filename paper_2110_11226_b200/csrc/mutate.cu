@@ -374,6 +374,29 @@ __global__ void emit_kernel(const gp_node* __restrict__ nodes, const int64_t* __
   }
 }
 
+// ---- initial population: ramped half-and-half ------------------
+// Program i: Full iff i < n / 2, max depth d_min + i mod (d_max - d_min + 1), its own Philox stream
+// (purpose 3, generation 0). Two passes over the same stream: the length, then the nodes.
+__global__ void init_len_kernel(int32_t n, MutConfig c, int32_t* __restrict__ lens) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  DevRng r(c.k0, c.k1, (uint32_t)i, 0u, 3u);
+  const int method = i < n / 2 ? FULL : GROW;
+  const int md = c.init_depth_min + i % (c.init_depth_max - c.init_depth_min + 1);
+  lens[i] = gen_program(r, method, md, c, [](int, gp_node) {});
+}
+
+__global__ void init_emit_kernel(int32_t n, MutConfig c, const int64_t* __restrict__ off,
+                                 gp_node* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  DevRng r(c.k0, c.k1, (uint32_t)i, 0u, 3u);
+  const int method = i < n / 2 ? FULL : GROW;
+  const int md = c.init_depth_min + i % (c.init_depth_max - c.init_depth_min + 1);
+  gp_node* o = out + off[i];
+  gen_program(r, method, md, c, [&](int k, gp_node nd) { o[k] = nd; });
+}
+
 // ---- stats of a population (engine.cpp evaluate(): histogram of variable-dependent nodes) -------
 __global__ void pop_stats_kernel(const gp_node* __restrict__ nodes, const int64_t* __restrict__ off,
                                  int32_t n, int32_t* __restrict__ depth_out, DevGenStats* st) {
@@ -489,6 +512,19 @@ cudaError_t launch_emit(const gp_node* nodes, const int64_t* off, int32_t n, uin
                         const MutConfig& c, const Recipe* recipes, const int64_t* out_off,
                         gp_node* out, cudaStream_t s) {
   emit_kernel<<<nblk(n, 64), 64, 0, s>>>(nodes, off, n, generation, c, recipes, out_off, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_lengths(int32_t n, const MutConfig& c, int32_t* lens, int64_t* off,
+                                cudaStream_t s) {
+  init_len_kernel<<<nblk(n, 64), 64, 0, s>>>(n, c, lens);
+  scan_kernel<int32_t, int64_t><<<1, 1024, 0, s>>>(lens, n, off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_emit(int32_t n, const MutConfig& c, const int64_t* off, gp_node* out,
+                             cudaStream_t s) {
+  init_emit_kernel<<<nblk(n, 64), 64, 0, s>>>(n, c, off, out);
   return cudaGetLastError();
 }
 

@@ -51,6 +51,11 @@ cudaError_t launch_plan(const gp_node* nodes, const int64_t* off, int32_t n, uin
 cudaError_t launch_emit(const gp_node* nodes, const int64_t* off, int32_t n, uint32_t generation,
                         const MutConfig& c, const Recipe* recipes, const int64_t* out_off,
                         gp_node* out, cudaStream_t s);
+// ramped half-and-half initial population: lengths + offsets (n + 1), then the nodes
+cudaError_t launch_init_lengths(int32_t n, const MutConfig& c, int32_t* lens, int64_t* off,
+                                cudaStream_t s);
+cudaError_t launch_init_emit(int32_t n, const MutConfig& c, const int64_t* off, gp_node* out,
+                             cudaStream_t s);
 cudaError_t launch_pop_stats(const gp_node* nodes, const int64_t* off, int32_t n, int32_t* depth,
                              DevGenStats* st, cudaStream_t s);
 cudaError_t launch_fit_stats(const float* fit, int32_t n, int32_t higher, const int64_t* off,
