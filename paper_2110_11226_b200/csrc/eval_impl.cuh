@@ -274,7 +274,10 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
         const bool in = i < nvalid;
         const int64_t row = t0 + i;
         if constexpr (!PREDICT) {
-          ys[i] = in ? a.y[row] : 0.0f;
+          // LogLoss stages the sign s = -1 (y > 1/2) / +1 instead of y: the per-row loss is then
+          // softplus(s yhat) (one multiply instead of a compare and a select)
+          const float yv = in ? a.y[row] : 0.0f;
+          ys[i] = a.metric == GP_LOGLOSS ? (in ? (yv > 0.5f ? -1.0f : 1.0f) : 0.0f) : yv;
           if (has_w) ws[i] = in ? a.w[row] : 0.0f;
         }
         if constexpr (XSMEM) {
@@ -290,6 +293,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
       // unweighted MSE / RMSE over a full tile: the FFMA-only loss, chosen once per tile
       const bool fast_mse = !PREDICT && (a.metric == GP_MSE || a.metric == GP_RMSE) && !has_w &&
                             nvalid == TILE;
+      const bool fast_ll = !PREDICT && a.metric == GP_LOGLOSS && !has_w && nvalid == TILE;
       // Single-sum metrics (A5): each lane stores its fp32 sum of a finished program into row
       // (slot % RR) of the warp's block; every RR programs the warp reduces the block at once --
       // LPR lanes per row each sum 32 / LPR values (LDS.128, conflict-free with the padded
@@ -326,6 +330,22 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
           fma_x2(l0, l1, d2, d3, d2, d3, l0, l1);
         }
       };
+      // unweighted LogLoss over a full tile: every row is live, ys holds the signs
+      auto loss_fast_ll = [&]() {
+#pragma unroll
+        for (int k = 0; k < R4; ++k) {
+          const float4 sv = *reinterpret_cast<const float4*>(ys + ebase + k * NT * 4);
+          float z[4];
+          mul_x2(z[0], z[1], st[0][4 * k], st[0][4 * k + 1], sv.x, sv.y);
+          mul_x2(z[2], z[3], st[0][4 * k + 2], st[0][4 * k + 3], sv.z, sv.w);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float l = fmaxf(z[j], 0.0f) + __logf(1.0f + __expf(-fabsf(z[j])));
+            l = fminf(fmaxf(l, kLogLossLo), kLogLossHi);
+            l0 += l;
+          }
+        }
+      };
       auto loss = [&](auto tag, float Kp) {
         constexpr int M = decltype(tag)::value;
 #pragma unroll
@@ -350,8 +370,8 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
               l0 += live ? ww[j] * fabsf(yh - yy[j]) : 0.0f;
             } else if constexpr (M == GP_LOGLOSS) {
               // -[y ln p + (1-y) ln(1-p)], p = sigmoid(yh), y in {0,1}: softplus(-+yh),
-              // clamped to the p-clamp's range (C7)
-              const float z = yy[j] > 0.5f ? -yh : yh;
+              // clamped to the p-clamp's range (C7); yy = the staged sign
+              const float z = yy[j] * yh;
               float l = fmaxf(z, 0.0f) + __logf(1.0f + __expf(-fabsf(z)));
               l = l < kLogLossLo ? kLogLossLo : (l > kLogLossHi ? kLogLossHi : l);
               l0 += live ? ww[j] * l : 0.0f;
@@ -379,6 +399,8 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
           }
         } else if (fast_mse) {
           loss_fast_mse();
+        } else if (fast_ll) {
+          loss_fast_ll();
         } else {
           switch (a.metric) {
             case GP_MAE: loss(MTag<GP_MAE>{}, 0.0f); break;
