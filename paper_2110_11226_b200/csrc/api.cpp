@@ -144,6 +144,11 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   const int64_t slots = (int64_t)sm_count(device) * occ_guess;
   const int64_t want_groups = std::max<int64_t>(1, (slots * 8 + n_tiles - 1) / n_tiles);
   int G = (int)std::min<int64_t>(g_max, std::max<int64_t>(1, (n_programs + want_groups - 1) / want_groups));
+  static const int env_G = [] {                                 // tuning knob GP_PLAN_G
+    const char* e = getenv("GP_PLAN_G");
+    return e && atoi(e) > 0 ? atoi(e) : 0;
+  }();
+  if (env_G > 0) G = std::min(env_G, g_max);
   if (force_G > 0) G = std::min(force_G, g_max);               // gp_context_set_plan
   const int n_groups = (n_programs + G - 1) / G;
   int64_t Q = std::min<int64_t>(n_tiles, std::max<int64_t>(1, (slots * per_slot + n_groups - 1) / n_groups));

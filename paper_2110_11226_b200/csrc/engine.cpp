@@ -313,6 +313,7 @@ struct gp_engine {
   bool dev_mut = false;
   bool host_view_valid = true;   // h_nodes / h_off / fit mirror the current population
   int32_t last_T = 0;            // tournaments of the last generation (device path)
+  bool sel_valid = false;        // d_kinds / d_win hold the last generation's selection
   StageBuf d_nodes2, d_off2, d_kinds, d_tcnt, d_toff, d_recipe, d_len, d_depth, d_stats;
   DevGenStats* h_stats = nullptr;  // pinned
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -607,6 +608,7 @@ struct gp_engine {
     std::swap(d_off, d_off2);
     n_nodes = total;
     last_T = T;
+    sel_valid = true;
     generation = (int)g;
     host_view_valid = false;
     pop.clear();                                   // the host copy is stale from here on
@@ -658,6 +660,7 @@ struct gp_engine {
     n_nodes = total;
     generation = 0;
     host_view_valid = false;
+    sel_valid = false;
     pop.clear();
     kinds.clear();
     winners.clear();
@@ -909,7 +912,13 @@ gp_status gp_engine_population_device(gp_engine* e, const gp_node** nodes,
 gp_status gp_engine_last_selection(gp_engine* e, const int32_t** kinds, const int32_t** winners,
                                    int32_t* n_tournaments) {
   if (!e) return GP_ERR_ARG;
-  if (e->dev_mut && e->generation > 0 && e->d_kinds.p) {
+  if (e->dev_mut) {
+    if (!e->sel_valid) {                 // no generation since init / set_population
+      e->kinds.clear();
+      e->winners.clear();
+    }
+  }
+  if (e->dev_mut && e->sel_valid && e->generation > 0 && e->d_kinds.p) {
     cudaSetDevice(e->ctx->device);
     const int n = e->cfg.population_size;
     e->kinds.resize(n);
@@ -955,6 +964,7 @@ gp_status gp_engine_set_population(gp_engine* e, const gp_node* nodes, const int
     e->n_nodes = n_nodes;
     e->generation = generation;
     e->host_view_valid = false;
+    e->sel_valid = false;
     e->pop.clear();
     if ((s = e->dev_stats(n))) return s;
     e->fill_stats_dev(&st);
@@ -980,6 +990,9 @@ gp_status gp_engine_set_population(gp_engine* e, const gp_node* nodes, const int
     }
     e->pop.swap(pop);
     e->generation = generation;
+    e->sel_valid = false;
+    e->kinds.clear();
+    e->winners.clear();
     if ((s = e->evaluate(&st, fitness))) return s;
     e->fill_stats(&st);
   }
