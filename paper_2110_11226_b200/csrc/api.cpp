@@ -199,6 +199,7 @@ static gp_status launch_variants(gp_context* ctx, EvalArgs a, const EvalPlan& pl
     a.prog_count = (const int32_t*)ctx->counts.p + v;
     a.work_counter = (int32_t*)ctx->counts.p + kNumVariants + v;
     a.part_base = (const int32_t*)ctx->inv.p + n + v;
+    a.group_size = (const int32_t*)ctx->inv.p + n + kNumVariants + 1 + v;
     const size_t smem = var.smem_bytes(pl.G, a.metric == GP_PEARSON ? 3 : 1, a.n_cols,
                                        a.w != nullptr, pl.xsmem, predict);
     const int occ = std::max(1, var.occupancy(predict, pl.xsmem, smem));
@@ -423,7 +424,7 @@ static gp_status prepare(gp_context* ctx, const gp_node*& programs, const int64_
   // stream words <= SUB_max x code words + 2 pad words
   if ((s = ctx->grow(&ctx->codestream.p, &ctx->codestream.cap, ((size_t)4 * (n_nodes + n) + 2) * sizeof(uint4), "stream"))) return s;
   if ((s = ctx->grow(&ctx->status.p, &ctx->status.cap, (size_t)n * sizeof(uint32_t), "status"))) return s;
-  if ((s = ctx->grow(&ctx->inv.p, &ctx->inv.cap, (size_t)(n + kNumVariants + 1) * sizeof(int32_t), "inv"))) return s;
+  if ((s = ctx->grow(&ctx->inv.p, &ctx->inv.cap, (size_t)(n + 2 * kNumVariants + 1) * sizeof(int32_t), "inv"))) return s;
   if ((s = ctx->grow(&ctx->scratch.p, &ctx->scratch.cap, (size_t)4 * n_nodes * sizeof(int32_t), "scratch"))) return s;
   if ((s = ctx->launch(launch_stage(programs, offsets, n_programs, n_nodes, n_cols, max_stack,
                                   (uint4*)ctx->code.p, (int64_t*)ctx->code_off.p,
@@ -483,8 +484,8 @@ static gp_status bucket_pack(gp_context* ctx, int32_t n_programs, int32_t G, boo
   return ctx->launch(launch_pack((const uint4*)ctx->code.p, (const int64_t*)ctx->code_off.p,
                                (const int32_t*)ctx->code_len.p, (const int32_t*)ctx->lists.p,
                                (const int64_t*)ctx->pos.p, counts, base,
-                               (const int64_t*)ctx->gstart.p, n_programs, G, subs,
-                               (uint4*)ctx->codestream.p, ctx->stream),
+                               (const int64_t*)ctx->gstart.p, n_programs, subs,
+                               (const int32_t*)ctx->inv.p, (uint4*)ctx->codestream.p, ctx->stream),
                    "pack kernel");
 }
 

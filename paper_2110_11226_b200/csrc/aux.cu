@@ -281,10 +281,25 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
     }
     __syncthreads();
   }
+  // per-bucket group size: as many groups as the plan gives the whole population (ceil(n / G)),
+  // so a small bucket (deep programs) is still spread over enough groups that the CTAs working on
+  // it share row chunks (a few large groups would keep ~CTAs / groups chunks of X in flight and
+  // spill L2: C5 generation 0's 8-slot launch re-read X from DRAM ~50 times)
+  // (only buckets that would get fewer than half the plan's groups are re-cut; the large ones
+  // keep G -- smaller groups there cost staging and measured slower on C3 / C4)
+  __shared__ int gsz_s[kNumVariants];
+  if (tid < kNumVariants) {
+    const int ng = (n + G - 1) / G;
+    const int groups_at_G = (cnt[tid] + G - 1) / G;
+    gsz_s[tid] = 2 * groups_at_G >= ng ? G : min(G, max(1, (cnt[tid] + ng - 1) / ng));
+    inv[n + kNumVariants + 1 + tid] = gsz_s[tid];
+  }
+  __syncthreads();
   // phase 2: stream offsets per bucket (words = SUB x (len + 1) per program)
   int64_t running = 0;
   for (int b = 0; b < kNumVariants; ++b) {
     const int cb = cnt[b];
+    const int Gb = gsz_s[b];
     if (tid == 0) base[b] = running;
     for (int c0 = 0; c0 < cb; c0 += 1024) {
       const int j = c0 + tid;
@@ -293,11 +308,11 @@ __global__ void __launch_bounds__(1024) bucket_kernel(const int32_t* __restrict_
       const int64_t tot = block_exclusive_scan(words, &ex, warp_tot);
       if (j < cb) {
         pos[(int64_t)b * n + j] = running + ex;
-        if (j % G == 0) gstart[(int64_t)b * (n + 1) + j / G] = running + ex;
+        if (j % Gb == 0) gstart[(int64_t)b * (n + 1) + j / Gb] = running + ex;
       }
       running += tot;
     }
-    if (tid == 0) gstart[(int64_t)b * (n + 1) + (cb + G - 1) / G] = running;
+    if (tid == 0) gstart[(int64_t)b * (n + 1) + (cb + Gb - 1) / Gb] = running;
     __syncthreads();
   }
   if (tid == 0) base[kNumVariants] = running;
@@ -333,7 +348,8 @@ __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __res
                             const int32_t* __restrict__ code_len, const int32_t* __restrict__ lists,
                             const int64_t* __restrict__ pos, const int32_t* __restrict__ counts,
                             const int64_t* __restrict__ base, const int64_t* __restrict__ gstart,
-                            int32_t n, int32_t G, int4 sub4, uint4* __restrict__ stream) {
+                            int32_t n, int4 sub4, const int32_t* __restrict__ inv,
+                            uint4* __restrict__ stream) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) stream[base[kNumVariants]] = stream[base[kNumVariants] + 1] = make_uint4(0, 0, 0, 0);
   if (i >= (int64_t)kNumVariants * n) return;
@@ -347,7 +363,8 @@ __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __res
   const int caps[kNumVariants] = {4, 8, 12, 20};   // kVariantStack
   const int vstack = caps[b];            // the variant's dispatch numbering (device_ops opv_rank)
   // the group's stream [gs, ge): words at window ends get kEndWin
-  const int64_t gs = gstart[(int64_t)b * (n + 1) + j / G], ge = gstart[(int64_t)b * (n + 1) + j / G + 1];
+  const int Gb = inv[n + kNumVariants + 1 + b];   // the bucket's group size (bucket_kernel)
+  const int64_t gs = gstart[(int64_t)b * (n + 1) + j / Gb], ge = gstart[(int64_t)b * (n + 1) + j / Gb + 1];
   for (int pass = 0; pass < subs[b]; ++pass) {
     for (int k = 0; k < len; ++k) {
       uint4 w = src[k];
@@ -356,7 +373,7 @@ __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __res
       *dst++ = w;
     }
     const bool last = pass == subs[b] - 1;
-    dst[-1].w = last ? (kEndProgram | ((uint32_t)(j % G) << 8))
+    dst[-1].w = last ? (kEndProgram | ((uint32_t)(j % Gb) << 8))
                      : (kEndPass | ((uint32_t)(pass + 1) << 8));
   }
   for (int64_t t = pos[i] - gs; t < pos[i] - gs + (int64_t)subs[b] * len; ++t)
@@ -366,15 +383,15 @@ __global__ void pack_kernel(const uint4* __restrict__ code, const int64_t* __res
 cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                         const int32_t* lists, const int64_t* pos, const int32_t* counts,
                         const int64_t* base, const int64_t* gstart, int32_t n_programs,
-                        int32_t G, const int* subs, uint4* stream, cudaStream_t s) {
+                        const int* subs, const int32_t* inv, uint4* stream, cudaStream_t s) {
   const int nt = 256;
   const int64_t total = (int64_t)kNumVariants * n_programs;
   pack_kernel<<<(unsigned)((total + nt - 1) / nt), nt, 0, s>>>(code, code_off, code_len, lists,
                                                                pos, counts, base, gstart,
-                                                               n_programs, G,
+                                                               n_programs,
                                                                make_int4(subs[0], subs[1], subs[2],
                                                                          subs[3]),
-                                                               stream);
+                                                               inv, stream);
   return cudaGetLastError();
 }
 

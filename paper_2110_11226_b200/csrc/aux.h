@@ -17,18 +17,20 @@ cudaError_t launch_stage(const gp_node* nodes, const int64_t* offsets, int32_t n
 // work counters. lists/pos: [kNumVariants][n_programs]; gstart: [kNumVariants][n_programs + 1];
 // counts: [kNumVariants] then counters [kNumVariants]; base: [kNumVariants + 1] stream bases;
 // inv: [n] compact partial-sum position of each program (-1: not evaluated), then
-// [kNumVariants + 1] bucket start positions and the evaluated total.
+// [kNumVariants + 1] bucket start positions and the evaluated total, then [kNumVariants] the
+// bucket group sizes (<= G: as many groups per bucket as the plan has for the population).
 cudaError_t launch_bucket(const int32_t* need, const int32_t* code_len, int32_t n_programs,
                           int32_t G, const int* subs, int32_t* lists, int64_t* pos,
                           int64_t* gstart, int32_t* counts, int64_t* base, int32_t skip_const,
-                          int32_t p_lo, int32_t p_hi, int32_t* inv /* n + kNumVariants + 1 */,
+                          int32_t p_lo, int32_t p_hi, int32_t* inv /* n + 2 kNumVariants + 1 */,
                           cudaStream_t s);
 // Copies every bucketed program's code into its variant stream, flagging the end of each pass
 // and of each shared-memory stream window (kernels.h kEndWin).
 cudaError_t launch_pack(const uint4* code, const int64_t* code_off, const int32_t* code_len,
                         const int32_t* lists, const int64_t* pos, const int32_t* counts,
                         const int64_t* base, const int64_t* gstart, int32_t n_programs,
-                        int32_t G, const int* subs, uint4* stream, cudaStream_t s);
+                        const int* subs, const int32_t* inv /* bucket group sizes at n + 5 */,
+                        uint4* stream, cudaStream_t s);
 // Dataset constants W, S_y, S_yy per row chunk -> partial[q][col0 .. col0 + 2].
 cudaError_t launch_consts(const float* y, const float* w, int64_t n_rows, int64_t rows_per_chunk,
                           int64_t n_chunks, const float* y_shift, double* partial, int64_t ld_part,

@@ -232,7 +232,12 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
   const int S = (a.metric == GP_PEARSON) ? 3 : 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int count = *a.prog_count;                 // programs in this variant's bucket
-  const int n_groups = (count + a.G - 1) / a.G;
+  // this bucket's group size (<= a.G; bucket_kernel), read once through shared memory
+  __shared__ int s_gv;
+  if (threadIdx.x == 0) s_gv = *a.group_size;
+  __syncthreads();
+  const int Gv = s_gv;
+  const int n_groups = (count + Gv - 1) / Gv;
   const int64_t n_items = (int64_t)n_groups * a.n_chunks;
   double* acc = reinterpret_cast<double*>(smem);                 // [NW][G][S]
   // this warp's transposed reduction block [RR][kRedStride] (single-sum metrics)
@@ -257,8 +262,8 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
     if (item >= n_items) break;
     const int g = (int)(item % n_groups);
     const int64_t q = item / n_groups;
-    const int np = min(a.G, count - g * a.G);
-    const int32_t* __restrict__ gids = a.prog_ids + (int64_t)g * a.G;   // group's program ids
+    const int np = min(Gv, count - g * Gv);
+    const int32_t* __restrict__ gids = a.prog_ids + (int64_t)g * Gv;    // group's program ids
     const int64_t s_begin = a.gstart[g], s_len = a.gstart[g + 1] - s_begin;
     if constexpr (!PREDICT) {
       for (int i = tid; i < NW * a.G * S; i += NT) acc[i] = 0.0;
@@ -473,7 +478,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
       // kConstCols + (part_base + j) * S (part_base = programs of the lower-capacity buckets), so
       // only programs that were evaluated per row are written and tile-reduced
       double* prow = a.partial + q * a.ld_part + kConstCols +
-                     ((int64_t)*a.part_base + (int64_t)g * a.G) * S;
+                     ((int64_t)*a.part_base + (int64_t)g * Gv) * S;
       for (int j = tid; j < np * S; j += NT) {
         const int pl = j / S, k = j - pl * S;
         double sum = 0.0;

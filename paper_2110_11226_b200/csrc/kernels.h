@@ -53,7 +53,8 @@ struct EvalArgs {
   int32_t n_cols;
   int32_t n_programs;
   int32_t metric;             // gp_metric
-  int32_t G;                  // programs per group
+  int32_t G;                  // programs per group: the plan's bound (shared-memory layout)
+  const int32_t* group_size;  // device: this variant's group size (<= G, bucket_kernel)
   int64_t rows_per_chunk;     // rows per work item (multiple of kTile)
   int64_t n_chunks;           // row chunks; work items = ceil(count / G) * n_chunks
   double* partial;            // FIT: [n_chunks][ld_part], ld_part = kConstCols + n_programs * S
