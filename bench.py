@@ -278,7 +278,7 @@ def run_b200(args, cfg):
     rows_local = X.shape[1] / (world if by_prog else 1)
 
     def step(e):
-        e.set_population(g0n, g0o, g0f, generation=0)
+        e.set_population(g0n, g0o, g0f, generation=0, stats=False)   # device copies, no sync
         return e.generation()
 
     def barrier():

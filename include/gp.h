@@ -347,7 +347,9 @@ gp_status gp_engine_population_device(gp_engine* e, const gp_node** nodes,
  * offsets[0] == 0) and declares it generation `generation`. fitness [host|device] fp32[n]: the
  * population's raw fitness, or NULL to evaluate it now. Programs must be valid with depth <=
  * stack_capacity - 1 (GP_ERR_ARG otherwise). Used to resume a run, to seed a population, and by
- * the benchmark to start every step from the same population. [sync] */
+ * the benchmark to start every step from the same population. [sync], except for a device
+ * population with device fitness on a device-mutation engine and stats_out == NULL: then the call
+ * only enqueues device-to-device copies on the context stream. */
 gp_status gp_engine_set_population(gp_engine* e, const gp_node* nodes, const int64_t* offsets,
                                    int32_t n_programs, int64_t n_nodes, const float* fitness,
                                    int32_t generation, gp_generation_stats* stats_out);

@@ -318,15 +318,19 @@ class Engine:
                    self.ctx.handle, "copy")
         return out_n, out_o, out_f
 
-    def set_population(self, nodes, offsets, fitness=None, generation: int = 0) -> dict:
-        """gp_engine_set_population ([host|device] flat CSR; fitness None = evaluate now)."""
+    def set_population(self, nodes, offsets, fitness=None, generation: int = 0,
+                       stats: bool = True):
+        """gp_engine_set_population ([host|device] flat CSR; fitness None = evaluate now).
+        stats=False skips the statistics (no synchronisation for device inputs); returns the
+        statistics dict or None."""
         self._keep_pop = (nodes, offsets, fitness)
         st = GpGenerationStats()
         _check(lib().gp_engine_set_population(self.handle, _ptr(nodes), _ptr(offsets),
                                               int(offsets.shape[0] - 1), int(nodes.shape[0]),
-                                              _ptr(fitness), int(generation), ctypes.byref(st)),
+                                              _ptr(fitness), int(generation),
+                                              ctypes.byref(st) if stats else None),
                self.ctx.handle, "gp_engine_set_population")
-        return st.as_dict()
+        return st.as_dict() if stats else None
 
     def last_selection(self):
         """(kinds int32 [n], winners int32 [T]) of the last gp_generation."""

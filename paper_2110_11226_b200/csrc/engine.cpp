@@ -966,6 +966,7 @@ gp_status gp_engine_set_population(gp_engine* e, const gp_node* nodes, const int
     e->host_view_valid = false;
     e->sel_valid = false;
     e->pop.clear();
+    if (!stats_out) return GP_OK;        // no statistics wanted: stream-ordered, no sync
     if ((s = e->dev_stats(n))) return s;
     e->fill_stats_dev(&st);
   } else {
