@@ -127,14 +127,19 @@ int gpb::sm_count(int device) {
 // items per slot. The plan counts every program, but variable-free programs skip the evaluator
 // (70 % of an evolved C3 population) and groups differ in total code length, so fine row chunks
 // keep the persistent CTAs' queue balanced to the end (C3 SFU frac: 0.72 at 8 items per slot,
-// 0.77 at 32, 0.79 at 128). All variants share the 2048-row tile.
+// 0.77 at 32, 0.79 at 128). Chunks are whole tiles of the plan tile (kernels.h); the slot count
+// assumes 4 resident 128-thread CTAs per SM (the shared-memory shapes run one 512-thread CTA per
+// SM, so each CTA takes ~4x the items; measured on C3 with the 512-thread s4, r02).
 EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t n_cols, int S,
                         bool predict, bool weighted, int force_G, int64_t force_tpc) {
   EvalPlan pl;
-  const int tile = kTile;
-  const int64_t n_tiles = (n_rows + tile - 1) / tile;
+  // X is staged in shared memory when the s4 shape's whole layout fits at the largest group
+  // (8192-row tiles, see kernels.h); otherwise the wide-dataset shapes read X through L1/L2
   const int g_max = 128;
-  pl.xsmem = (size_t)n_cols * tile * sizeof(float) <= 96 * 1024;
+  pl.xsmem = eval_variant_s4().smem_bytes(g_max, S, n_cols, weighted, 1, predict) <=
+             (size_t)kMaxDynSmem;
+  const int tile = pl.xsmem ? kTileSmem : kTile;
+  const int64_t n_tiles = (n_rows + tile - 1) / tile;
   const int occ_guess = 4;
   // row-chunk items per resident CTA slot (tuning knob GP_ITEMS_PER_SLOT)
   static const int per_slot = [] {
@@ -155,14 +160,15 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   int64_t tpc = (n_tiles + Q - 1) / Q;
   if (force_tpc > 0) tpc = std::min<int64_t>(force_tpc, n_tiles);
   Q = (n_tiles + tpc - 1) / tpc;
+  static const int env_order = [] {                             // tuning knob GP_ITEM_ORDER
+    const char* e = getenv("GP_ITEM_ORDER");
+    return e ? atoi(e) : 0;
+  }();
+  pl.item_order = env_order;
   pl.G = G;
   pl.n_groups = n_groups;
   pl.n_chunks = Q;
   pl.rows_per_chunk = tpc * tile;
-  const size_t yw = predict ? 0 : (weighted ? 2 : 1) * (size_t)tile * sizeof(float);
-  // tiles + stream window; each variant adds its accumulator / reduction block bytes at launch
-  pl.smem = yw + (pl.xsmem ? (size_t)n_cols * tile * sizeof(float) : 0) +
-            (size_t)(kStreamWin + 2) * 16;
   return pl;
 }
 
@@ -194,6 +200,7 @@ static gp_status launch_variants(gp_context* ctx, EvalArgs a, const EvalPlan& pl
     if (var.shape.SUB != variant(v).shape.SUB)   // the pack kernel laid out SUB copies per program
       return ctx->fail(GP_ERR_ARG, "evaluator variant %d: wide shape SUB mismatch", v);
     a.stream = (const uint4*)ctx->codestream.p;
+    a.item_order = pl.item_order;
     a.gstart = (const int64_t*)ctx->gstart.p + (int64_t)v * (n + 1);
     a.prog_ids = (const int32_t*)ctx->lists.p + (int64_t)v * n;
     a.prog_count = (const int32_t*)ctx->counts.p + v;

@@ -59,7 +59,11 @@ namespace GP_NS {
 
 constexpr int STACK = GP_STACK, R = GP_R, SUB = GP_SUB, NT = GP_NT;
 constexpr int TILE = NT * R * SUB;
-static_assert(TILE == kTile, "every variant shares the row tile");
+#ifdef GP_GLOBAL_X_ONLY
+static_assert(TILE == kTile, "wide-dataset shapes work on the 2048-row plan tile");
+#else
+static_assert(TILE == kTileSmem, "shared-memory-X shapes stage the 8192-row plan tile");
+#endif
 constexpr int NW = NT / 32, R4 = R / 4;
 constexpr int RR = GP_RED_ROWS, LPR = 32 / RR, RED_BYTES = NW * RR * kRedStride * 4;
 static_assert(RR == 8 || RR == 16, "reduction block: 8 or 16 programs");
@@ -67,8 +71,6 @@ static_assert(R % 4 == 0 && NT % 32 == 0, "R must be a multiple of 4");
 static_assert(STACK <= kCaseStride, "slot must fit the case stride");
 static_assert(opv_rank(OPV_COUNT - 1) < OPV_COUNT, "opv_rank is a permutation of 0..OPV_COUNT-1");
 
-// dynamic shared-memory opt-in: 227 KB per CTA minus the kernel's static shared memory
-constexpr int kMaxDynSmem = 220 * 1024;
 static_assert(kStreamWin % 4 == 0, "stream window");
 
 constexpr float kLogLossLo = 1.0000000000000005e-15f;  // -ln(1 - 1e-15), S:191 clamp (C7)
@@ -77,8 +79,12 @@ constexpr float kLogLossHi = 34.538776394910684f;      // -ln(1e-15)
 // Shared-memory layout (bytes): fp64 accumulators [NW][G][S] | reduction blocks [NW][kRedRows]
 // [kRedStride] fp32 | ys[TILE] | ws[TILE] (weighted only) | xs[n_cols][TILE] (small n_cols only)
 // | code-stream window [kStreamWin + 2] uint4
+// (the reduction blocks serve the single-sum metrics only: Pearson reduces by warp shuffles)
+__host__ __device__ inline size_t smem_fp64_bytes(int G, int S) {
+  return ((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15;
+}
 __host__ __device__ inline size_t smem_acc_bytes(int G, int S) {
-  return (((size_t)NW * G * S * sizeof(double) + 15) & ~(size_t)15) + RED_BYTES;
+  return smem_fp64_bytes(G, S) + (S == 1 ? RED_BYTES : 0);
 }
 // Dynamic shared memory of one launch of this shape.
 inline size_t smem_total(int G, int S, int n_cols, bool weighted, bool xsmem, bool predict) {
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
   const int64_t n_items = (int64_t)n_groups * a.n_chunks;
   double* acc = reinterpret_cast<double*>(smem);                 // [NW][G][S]
   // this warp's transposed reduction block [RR][kRedStride] (single-sum metrics)
-  float* rbw = reinterpret_cast<float*>(smem + (PREDICT ? 0 : smem_acc_bytes(a.G, S) - RED_BYTES)) +
+  float* rbw = reinterpret_cast<float*>(smem + (PREDICT ? 0 : smem_fp64_bytes(a.G, S))) +
                warp * (RR * kRedStride);
   const bool has_w = a.w != nullptr;
   // global-X path: 16-byte vector loads when every column start is 16-byte aligned
@@ -260,8 +266,8 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
     __syncthreads();
     const int64_t item = s_item;
     if (item >= n_items) break;
-    const int g = (int)(item % n_groups);
-    const int64_t q = item / n_groups;
+    const int g = a.item_order ? (int)(item / a.n_chunks) : (int)(item % n_groups);
+    const int64_t q = a.item_order ? item % a.n_chunks : item / n_groups;
     const int np = min(Gv, count - g * Gv);
     const int32_t* __restrict__ gids = a.prog_ids + (int64_t)g * Gv;    // group's program ids
     const int64_t s_begin = a.gstart[g], s_len = a.gstart[g + 1] - s_begin;

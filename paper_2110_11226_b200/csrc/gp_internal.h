@@ -19,7 +19,7 @@ struct EvalPlan {
   bool xsmem = true;
   int G = 1, n_groups = 1, occupancy = 1;
   int64_t n_chunks = 1, rows_per_chunk = 0;
-  size_t smem = 0;
+  int item_order = 0;        // 0: program group fastest, 1: row chunk fastest (EvalArgs)
 };
 
 bool is_host_pointer(const void* p);

@@ -10,8 +10,14 @@ namespace gpb {
 // Case ids of the compiled code use ONE slot stride for every evaluator variant (so the stage
 // kernel is variant independent): case id = opv * kCaseStride + slot.
 constexpr int kCaseStride = GP_MAX_STACK;
-// Row tile of every variant (NT * R * SUB = 2048) -> one work decomposition for all variants.
+// Row tiles (NT * R * SUB): the shared-memory-X shapes s4..s20 (512 threads) stage 8192-row
+// tiles; the wide-dataset shapes w4 / w8 (global-memory X) work on 2048-row tiles. Row chunks are
+// whole tiles of the plan's tile (kTileSmem when X is staged in shared memory, else kTile).
 constexpr int kTile = 2048;
+constexpr int kTileSmem = 8192;
+// Dynamic shared-memory opt-in of the evaluator kernels (227 KB per CTA minus the kernels' 16 B of
+// static shared memory, rounded down).
+constexpr int kMaxDynSmem = 227 * 1024 - 256;
 // Evaluator variants by register-stack capacity; program p runs in the first variant whose
 // capacity >= its stack need (bucketed on the device, no host synchronisation).
 constexpr int kNumVariants = 4;
@@ -55,8 +61,9 @@ struct EvalArgs {
   int32_t metric;             // gp_metric
   int32_t G;                  // programs per group: the plan's bound (shared-memory layout)
   const int32_t* group_size;  // device: this variant's group size (<= G, bucket_kernel)
-  int64_t rows_per_chunk;     // rows per work item (multiple of kTile)
+  int64_t rows_per_chunk;     // rows per work item (whole plan tiles)
   int64_t n_chunks;           // row chunks; work items = ceil(count / G) * n_chunks
+  int32_t item_order;         // work-item order: 0 = program group fastest, 1 = row chunk fastest
   double* partial;            // FIT: [n_chunks][ld_part], ld_part = kConstCols + n_programs * S
   int64_t ld_part;
   const int32_t* part_base;   // FIT, device: first compact partial slot of this variant's bucket

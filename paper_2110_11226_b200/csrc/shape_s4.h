@@ -1,8 +1,10 @@
 // Evaluator variant: register stack of 4 slots, 16 rows per thread per pass, 1 pass per tile,
-// 128-register budget (4 CTAs per SM): measured best on C3 (DESIGN.md performance log).
+// 512-thread CTAs at the 128-register budget (1 CTA = 16 warps per SM). One CTA per SM means the
+// four warps on each SM sub-partition walk the SAME code stream, so the leading warp's
+// instruction-cache misses are the followers' hits (4 CTAs of 128 threads walked 4 different
+// streams: gen-0 C3 gp_evaluate 224 -> 197 ms, step 134 -> 128 ms; profiles/ab_r02_nt512.log).
 #define GP_STACK 4
 #define GP_R 16
 #define GP_SUB 1
-#define GP_NT 128
-#define GP_MINB 4
-
+#define GP_NT 512
+#define GP_MINB 1

@@ -3,7 +3,7 @@
 Small parity tests run at sizes where the planner picks one or two programs per group and one tile
 per work item. Here the plan is forced to the shape the benchmark runs (gp_context_set_plan):
 groups of 128 programs (full 16-program reduction blocks, code streams longer than the 768-word
-shared-memory window) and 7-tile row chunks with a ragged last chunk and tile, and EVERY program is
+shared-memory window) and 3-tile row chunks with a ragged last chunk and tile, and EVERY program is
 compared with the oracle for all five metrics, unweighted and weighted with exact zeros (SURVEY
 rows A2-A5, A7).
 
@@ -22,7 +22,7 @@ from tests.test_gpu_parity import _dataset, check_fitness, dev
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-ROWS = 253 * 253          # 64,009 rows = 31 tiles of 2048 + a ragged tile of 1,521 rows
+ROWS = 253 * 253          # 64,009 rows = 7 tiles of 8192 + a ragged tile of 6,665 rows
 METRICS = ["mae", "mse", "rmse", "logloss", "pearson"]
 
 
@@ -78,8 +78,8 @@ def _case(orc, cache, metric, weighted):
 @pytest.mark.parametrize("metric", METRICS)
 def test_production_plan_every_program(gp, pctx, orc, oracle_cache, metric, weighted):
     X, y, w, nodes, off, ref, sens, flags = _case(orc, oracle_cache, metric, weighted)
-    assert X.shape[1] % 2048 != 0
-    pctx.set_plan(128, 7)                       # 128-program groups, 7-tile chunks (5 chunks)
+    assert X.shape[1] % 8192 != 0
+    pctx.set_plan(128, 3)                       # 128-program groups, 3-tile chunks (3 chunks)
     fit, st = pctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), None if w is None else dev(w),
                             metric=metric, max_stack=8)
     torch.cuda.synchronize()
@@ -104,7 +104,7 @@ def test_production_plan_deep_buckets(gp, pctx, orc, metric):
     X, y = _dataset(metric, 40_000, seed=13)
     nodes, off = synth.deep_population(400, seed=5, need=(9, 20), n_features=X.shape[0])
     pctx.set_eval_order(False)
-    pctx.set_plan(128, 5)
+    pctx.set_plan(128, 2)                       # 8192-row tiles: 2 chunks, the last ragged
     fit, st = pctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), metric=metric, max_stack=20)
     ref, sens, flags = orc.population_fitness(nodes, off, X, y, None, metric)
     check_fitness(fit.cpu().numpy(), ref, sens, flags, metric, label=f"deep production {metric}")
@@ -209,10 +209,10 @@ def test_partial_rejects_spearman(gp, pctx):
 
 @pytest.mark.parametrize("metric", METRICS)
 def test_wide_dataset_every_program(gp, pctx, orc, metric):
-    """Wide datasets (> 11 columns: no 2048-row shared-memory X tile) run the warp-per-program
-    kernels (w4 / w8: one warp's rows staged for every column, programs handed to warps from a
-    shared counter): every program against the oracle, weighted with exact zeros, ragged tail,
-    both the 4- and the 8-slot shape (classic order keeps the deep needs), at the production plan."""
+    """Wide datasets (no 8192-row shared-memory X tile fits) read X through L1/L2 in the wide
+    shapes w4 / w8 (2048-row tiles): every program against the oracle, weighted with exact zeros,
+    ragged tail, both the 4- and the 8-slot shape (classic order keeps the deep needs), at the
+    production plan."""
     n_rows, n_cols = 20_000 + 77, 40
     Xh, yh = synth.higgs_like(n_rows, seed=21, n_cols=n_cols)
     if metric != "logloss":

@@ -21,6 +21,8 @@ F_OVF, F_AMB, F_INV, F_UND = 1, 2, 4, 8
 # fitness beyond which an fp32 lane sum of <= 256 rows with weights < 2 may overflow
 FP32_SUM_LIMIT = float(np.finfo(np.float32).max) / 512
 # Tolerance model: DESIGN.md "Tolerance model" (north_star: relative 1e-4 in fp32).
+# row tile of the shared-memory-X evaluator shapes (kernels.h kTileSmem)
+SMEM_TILE = 8192
 
 
 @pytest.fixture(scope="module")
@@ -131,7 +133,7 @@ def check_fitness(gpu_fit, ref, sens, flags, metric, max_excluded=0.03, max_ill=
 def test_predict_rows_match_oracle(gp, ctx, orc, funcs, max_stack, depth):
     nodes, off = synth.random_population(120, seed=max_stack + len(funcs), depth=depth,
                                          funcs=funcs, max_stack=max_stack, p_terminal=0.25)
-    X, _ = synth.pagie_grid(48)            # 2304 rows: one full tile + ragged tail (s8 tile 2048)
+    X, _ = synth.pagie_grid(96)            # 9216 rows: one full 8192-row tile + ragged tail
     out, st = ctx.predict(dev(nodes), dev(off), dev(X), max_stack=max_stack)
     torch.cuda.synchronize()
     assert (st.cpu().numpy() == 0).all()
@@ -251,7 +253,7 @@ def _dataset(metric, n_rows, seed=0):
 @pytest.mark.parametrize("metric", ["mae", "mse", "rmse", "logloss", "pearson"])
 @pytest.mark.parametrize("weighted", [False, True])
 def test_evaluate_fitness_matches_oracle(gp, ctx, orc, metric, weighted):
-    n_rows = 3 * 2048 + 37                  # several tiles + ragged tail
+    n_rows = 2 * SMEM_TILE + 37             # several tiles + ragged tail
     X, y = _dataset(metric, n_rows, seed=3)
     n_feat = X.shape[0]
     nodes, off = synth.random_population(160, seed=100 + len(metric), depth=(0, 6),
@@ -429,7 +431,7 @@ def test_constant_programs_match_oracle(gp, ctx, orc, metric, weighted):
     """Variable-free programs skip the per-row evaluator for MSE / RMSE / Pearson (closed form
     from W, S_y, S_yy); every metric must still match the oracle, and the closed form must
     agree with the per-row evaluation of the same programs."""
-    n_rows = 2 * 2048 + 999
+    n_rows = 2 * SMEM_TILE + 999
     X, y = _dataset(metric, n_rows, seed=8)
     nodes, off = _constant_heavy_population(200, seed=31)
     w = synth.weights(n_rows, seed=6) if weighted else None
@@ -469,7 +471,7 @@ def _integer_case(n_rows, n_prog, seed):
 @pytest.mark.parametrize("weighted", [False, True])
 @pytest.mark.parametrize("batch", [None, 7])
 def test_spearman_exact_inputs_match_oracle(gp, ctx, orc, weighted, batch, monkeypatch):
-    n_rows = 2 * 2048 + 999
+    n_rows = 2 * SMEM_TILE + 999
     X, y, nodes, off = _integer_case(n_rows, 90, seed=12)
     w = synth.weights(n_rows, seed=3) if weighted else None
     if batch:

@@ -6,7 +6,8 @@
 Each experiment recompiles the kernels of ONE shape (the shape_<v>.h macros replaced; one
 translation unit per (PREDICT, XSMEM) as in build.py) and links them with the in-tree objects of
 everything else into paper_2110_11226_b200/_exp/libgp_<name>.so (GP_B200_LIB selects it at run
-time). The shape must keep NT * R * SUB = 2048 and the SUB of its s/w partner.
+time). The shape must keep its tile NT * R * SUB (8192 for s4..s20, 2048 for w4 / w8) and the SUB
+of its s/w partner.
 """
 import concurrent.futures as cf
 import os
