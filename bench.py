@@ -54,12 +54,13 @@ CONFIGS = {
                data="year", rows=1_048_576, pop=8192, metric="rmse", depth=(2, 8)),
 }
 # Algorithmic SFU (MUFU) operations per node-row: the transcendental /
-# reciprocal evaluations the method itself requires, whatever the implementation. Counted only
-# for nodes whose subtree depends on a variable (stats op_count); variable-free subtrees are
-# per-program constants, not per-row work.
-SFU_COST = {5: 1, 9: 1, 10: 1, 11: 3, 14: 1, 15: 1, 16: 1, 17: 1, 8: 2, 20: 2, 21: 2, 22: 2,
+# reciprocal evaluations each function needs at the least (tan = one reciprocal after a range
+# reduction and a polynomial, 13 FP32 ops; sin / cos one MUFU each). Counted only for nodes whose
+# subtree depends on a variable (stats op_count); variable-free subtrees are per-program
+# constants, not per-row work.
+SFU_COST = {5: 1, 9: 1, 10: 1, 11: 1, 14: 1, 15: 1, 16: 1, 17: 1, 8: 2, 20: 2, 21: 2, 22: 2,
             23: 1, 24: 1, 25: 1}
-FP32_COST = {2: 1, 3: 1, 4: 1, 5: 1, 6: 1, 7: 1, 9: 1, 10: 1, 11: 2, 12: 1, 13: 1, 18: 1, 19: 2}
+FP32_COST = {2: 1, 3: 1, 4: 1, 5: 1, 6: 1, 7: 1, 9: 1, 10: 1, 11: 13, 12: 1, 13: 1, 18: 1, 19: 2}
 LOSS_FP32 = {"mae": 3, "mse": 3, "rmse": 3, "logloss": 7, "pearson": 5}
 LOSS_SFU = {"logloss": 2}
 # B200: 148 SMs x 16 MUFU lanes x 1965 MHz (sm_max_mhz); microbenchmarked 4.63e12 MUFU.SIN/s

@@ -142,11 +142,48 @@ __device__ __forceinline__ float apply2(float a, float b) {
   }
 }
 
+// tan on the FMA pipe plus ONE MUFU.RCP (GP_TAN_POLY = 1, default) instead of sin, cos and rcp
+// (3 MUFU): x = k pi/2 + r with k = rint(2x/pi) (the 1.5 * 2^23 magic addition; bit 0 of the sum
+// is k's parity) and r by a three-constant FMA Cody-Waite reduction (|r| <= pi/4); tan r =
+// r + r z P(z), z = r^2, P the degree-5 minimax fit of (tan r / r - 1) / z on [0, (pi/4)^2]
+// (tools/tan_fit.py: 1.8e-8 relative; the coefficients agree with Cephes tanf); tan x = tan r for
+// even k, -1 / tan r for odd k. numpy emulation of this FFMA sequence (tools/tan_fit.py): <= 3 ulp
+// for |x| < 1e3 and <= 0.12 of the oracle's tan budget for |x| up
+// to 3e6; beyond 2^22 pi/2 the magic rounding fails and the budget is infinite (excluded).
+#ifndef GP_TAN_POLY
+#define GP_TAN_POLY 1
+#endif
+constexpr float kTanMagic = 12582912.0f, kTwoOverPi = 0.636619772f;
+constexpr float kPio2A = 1.5707964f, kPio2B = -4.371139e-08f, kPio2C = -1.7763568e-15f;
+constexpr float kTanP0 = 0.33333156f, kTanP1 = 0.133388f, kTanP2 = 0.053411208f,
+                kTanP3 = 0.024430392f, kTanP4 = 0.0031195127f, kTanP5 = 0.009385642f;
+__device__ __forceinline__ float tan_poly(float x) {
+  const float j = fmaf(x, kTwoOverPi, kTanMagic);
+  const float k = j - kTanMagic;
+  float r = fmaf(k, -kPio2A, x);
+  r = fmaf(k, -kPio2B, r);
+  r = fmaf(k, -kPio2C, r);
+  const float z = r * r;
+  float p = fmaf(kTanP5, z, kTanP4);
+  p = fmaf(p, z, kTanP3);
+  p = fmaf(p, z, kTanP2);
+  p = fmaf(p, z, kTanP1);
+  p = fmaf(p, z, kTanP0);
+  const float t = fmaf(r * z, p, r);
+  const float u = rcp_approx(-t);
+  return (__float_as_int(j) & 1) ? u : t;
+}
 template <int OP>
 __device__ __forceinline__ float apply1(float a) {
   if constexpr (OP == GP_OP_SIN) return __sinf(a);
   else if constexpr (OP == GP_OP_COS) return __cosf(a);
-  else if constexpr (OP == GP_OP_TAN) return __sinf(a) * rcp_fast(__cosf(a));
+  else if constexpr (OP == GP_OP_TAN) {
+#if GP_TAN_POLY
+    return tan_poly(a);
+#else
+    return __sinf(a) * rcp_fast(__cosf(a));
+#endif
+  }
   else if constexpr (OP == GP_OP_ABS) return fabsf(a);
   else if constexpr (OP == GP_OP_NEG) return -a;
   else if constexpr (OP == GP_OP_SQRT) return sqrt_approx(fabsf(a));
@@ -209,6 +246,27 @@ __device__ __forceinline__ void rcp_fast_x2(float& r0, float& r1, float b0, floa
 #endif
 }
 
+// tan_poly on two rows (FFMA2 / FMUL2 / FADD2), bit-identical to two tan_poly calls
+__device__ __forceinline__ void tan_poly_x2(float& d0, float& d1, float x0, float x1) {
+  float j0, j1, k0, k1, r0, r1, z0, z1, p0, p1, q0, q1;
+  fma_x2(j0, j1, x0, x1, kTwoOverPi, kTwoOverPi, kTanMagic, kTanMagic);
+  sub_x2(k0, k1, j0, j1, kTanMagic, kTanMagic);
+  fma_x2(r0, r1, k0, k1, -kPio2A, -kPio2A, x0, x1);
+  fma_x2(r0, r1, k0, k1, -kPio2B, -kPio2B, r0, r1);
+  fma_x2(r0, r1, k0, k1, -kPio2C, -kPio2C, r0, r1);
+  mul_x2(z0, z1, r0, r1, r0, r1);
+  fma_x2(p0, p1, kTanP5, kTanP5, z0, z1, kTanP4, kTanP4);
+  fma_x2(p0, p1, p0, p1, z0, z1, kTanP3, kTanP3);
+  fma_x2(p0, p1, p0, p1, z0, z1, kTanP2, kTanP2);
+  fma_x2(p0, p1, p0, p1, z0, z1, kTanP1, kTanP1);
+  fma_x2(p0, p1, p0, p1, z0, z1, kTanP0, kTanP0);
+  mul_x2(q0, q1, r0, r1, z0, z1);
+  fma_x2(q0, q1, q0, q1, p0, p1, r0, r1);
+  const float u0 = rcp_approx(-q0), u1 = rcp_approx(-q1);
+  d0 = (__float_as_int(j0) & 1) ? u0 : q0;
+  d1 = (__float_as_int(j1) & 1) ? u1 : q1;
+}
+
 // apply2 on two rows: (d0, d1) = (a0 OP b0, a1 OP b1), bit-identical to two apply2 calls.
 template <int OP>
 __device__ __forceinline__ void apply2_x2(float& d0, float& d1, float a0, float a1, float b0,
@@ -237,9 +295,13 @@ __device__ __forceinline__ void apply1_x2(float& d0, float& d1, float a0, float 
     mul_x2(s0, s1, a0, a1, a0, a1);
     mul_x2(d0, d1, s0, s1, a0, a1);
   } else if constexpr (OP == GP_OP_TAN) {
+#if GP_TAN_POLY
+    tan_poly_x2(d0, d1, a0, a1);
+#else
     float i0, i1;
     rcp_fast_x2(i0, i1, __cosf(a0), __cosf(a1));
     mul_x2(d0, d1, __sinf(a0), __sinf(a1), i0, i1);
+#endif
   } else if constexpr (OP == GP_OP_INV) {
     float i0, i1;
     rcp_fast_x2(i0, i1, a0, a1);
