@@ -94,6 +94,19 @@ inline size_t smem_total(int G, int S, int n_cols, bool weighted, bool xsmem, bo
 }
 
 #define LBL(OPV, s) (opv_rank(OPV) * STACK + (s))   // pack_kernel's numbering
+// End of a case. GP_CASE_CONTINUE = 1 (default): an unflagged word (the common case) continues
+// with the next dispatch straight from the case (one taken branch per word instead of two: case ->
+// shared tail -> loop head); C3 step 123.2 -> 121.2 ms (profiles/ab_r02_dispatch.log). The
+// compiled loop head then also rotates the two prefetched case ids without waiting on the LDS.
+// (GP_PREFETCH = 1, a one-deep id prefetch, was measured slower: 125.5 ms.)
+#ifndef GP_CASE_CONTINUE
+#define GP_CASE_CONTINUE 1
+#endif
+#if GP_CASE_CONTINUE
+#define GP_BRK if (cw.w == 0u) continue; break;
+#else
+#define GP_BRK break;
+#endif
 
 // -- dispatch cases -------------------------------------------------------------------------------
 // Cases work on 4-row chunks (one LDS.128 of a variable per chunk), so a fused variable operand
@@ -143,39 +156,39 @@ inline size_t smem_total(int G, int S, int n_cols, bool weighted, bool xsmem, bo
 #define GP_ST2(s) st[s][r], st[s][r + 1]
 
 #define GP_PUSH(s)                                                                             \
-  case LBL(OPV_PUSH_V, s): { GP_CHUNKS(GP_VAR4(t, cw.y, k), st[s][r] = GP_F4(t)) } break;      \
-  case LBL(OPV_PUSH_C, s): { const float c = GP_CONST(cw.y); GP_ROWS(st[s][r] = c) } break;
+  case LBL(OPV_PUSH_V, s): { GP_CHUNKS(GP_VAR4(t, cw.y, k), st[s][r] = GP_F4(t)) } GP_BRK      \
+  case LBL(OPV_PUSH_C, s): { const float c = GP_CONST(cw.y); GP_ROWS(st[s][r] = c) } GP_BRK
 
 // binary op OP at destination slot s; a = first operand, b = second operand
 #define GP_BIN_SS(OP, s)                                                                       \
   case LBL(opv_bin(OP, BV_SS), s): {                                                           \
-    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), GP_ST2((s) + 1), GP_ST2(s))) } break;                    \
+    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), GP_ST2((s) + 1), GP_ST2(s))) } GP_BRK                    \
   case LBL(opv_bin(OP, BV_SSR), s): {                                                          \
-    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), GP_ST2(s), GP_ST2((s) + 1))) } break;
+    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), GP_ST2(s), GP_ST2((s) + 1))) } GP_BRK
 #define GP_BIN_T(OP, s)                                                                        \
   case LBL(opv_bin(OP, BV_SV), s): {                                                           \
-    GP_CHUNKS2(GP_VAR4(t, cw.z, k), apply2_x2<OP>(GP_ST2(s), GP_ST2(s), GP_LO(t), GP_HI(t))) } break; \
+    GP_CHUNKS2(GP_VAR4(t, cw.z, k), apply2_x2<OP>(GP_ST2(s), GP_ST2(s), GP_LO(t), GP_HI(t))) } GP_BRK \
   case LBL(opv_bin(OP, BV_SC), s): { const float c = GP_CONST(cw.z);                           \
-    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), GP_ST2(s), c, c)) } break;                               \
+    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), GP_ST2(s), c, c)) } GP_BRK                               \
   case LBL(opv_bin(OP, BV_VS), s): {                                                           \
-    GP_CHUNKS2(GP_VAR4(t, cw.y, k), apply2_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t), GP_ST2(s))) } break; \
+    GP_CHUNKS2(GP_VAR4(t, cw.y, k), apply2_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t), GP_ST2(s))) } GP_BRK \
   case LBL(opv_bin(OP, BV_CS), s): { const float c = GP_CONST(cw.y);                           \
-    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), c, c, GP_ST2(s))) } break;                               \
+    GP_PAIRS(apply2_x2<OP>(GP_ST2(s), c, c, GP_ST2(s))) } GP_BRK                               \
   case LBL(opv_bin(OP, BV_VV), s): {                                                           \
     GP_CHUNKS2(GP_VAR4(t, cw.y, k) GP_VAR4(u, cw.z, k),                                        \
-               apply2_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t), GP_LO(u), GP_HI(u))) } break;      \
+               apply2_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t), GP_LO(u), GP_HI(u))) } GP_BRK      \
   case LBL(opv_bin(OP, BV_VC), s): { const float c = GP_CONST(cw.z);                           \
-    GP_CHUNKS2(GP_VAR4(t, cw.y, k), apply2_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t), c, c)) } break; \
+    GP_CHUNKS2(GP_VAR4(t, cw.y, k), apply2_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t), c, c)) } GP_BRK \
   case LBL(opv_bin(OP, BV_CV), s): { const float c = GP_CONST(cw.y);                           \
-    GP_CHUNKS2(GP_VAR4(u, cw.z, k), apply2_x2<OP>(GP_ST2(s), c, c, GP_LO(u), GP_HI(u))) } break; \
+    GP_CHUNKS2(GP_VAR4(u, cw.z, k), apply2_x2<OP>(GP_ST2(s), c, c, GP_LO(u), GP_HI(u))) } GP_BRK \
   case LBL(opv_bin(OP, BV_CC), s): {                                                           \
-    const float v = apply2<OP>(GP_CONST(cw.y), GP_CONST(cw.z)); GP_ROWS(st[s][r] = v) } break;
+    const float v = apply2<OP>(GP_CONST(cw.y), GP_CONST(cw.z)); GP_ROWS(st[s][r] = v) } GP_BRK
 #define GP_UN(OP, s)                                                                           \
-  case LBL(opv_un(OP, UV_S), s): { GP_PAIRS(apply1_x2<OP>(GP_ST2(s), GP_ST2(s))) } break;      \
+  case LBL(opv_un(OP, UV_S), s): { GP_PAIRS(apply1_x2<OP>(GP_ST2(s), GP_ST2(s))) } GP_BRK      \
   case LBL(opv_un(OP, UV_V), s): {                                                             \
-    GP_CHUNKS2(GP_VAR4(t, cw.y, k), apply1_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t))) } break;     \
+    GP_CHUNKS2(GP_VAR4(t, cw.y, k), apply1_x2<OP>(GP_ST2(s), GP_LO(t), GP_HI(t))) } GP_BRK     \
   case LBL(opv_un(OP, UV_C), s): { const float v = apply1<OP>(GP_CONST(cw.y));                 \
-    GP_ROWS(st[s][r] = v) } break;
+    GP_ROWS(st[s][r] = v) } GP_BRK
 
 // Every case whose destination slot is s (SS needs slot s + 1 as well), listed as the paper's
 // function set (Table 2 / 6: add, sub, mul, div, sin, cos, tan) and the rest of the
@@ -435,12 +448,24 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
         // at the top of each iteration (its LDS latency overlaps the dispatch branch). The loop
         // has no trip counter: the window's last word carries kEndWin (pack_kernel).
         const uint4* wp = sw;
+#ifndef GP_PREFETCH
+#define GP_PREFETCH 2
+#endif
+#if GP_PREFETCH == 2
         uint32_t c_n = wp[0].x, c_n2 = wp[1].x;
+#else
+        uint32_t c_n = wp[0].x;
+#endif
 #pragma unroll 1
         for (;;) {
           const uint32_t cid = c_n;
+#if GP_PREFETCH == 2
           c_n = c_n2;
           c_n2 = wp[2].x;                            // window carries two look-ahead words
+#else
+          c_n = wp[1].x;                             // loaded into the register the next dispatch
+                                                     // reads: no rotation move before the BRX
+#endif
           const uint4 cw = *wp;
           ++wp;
           switch (cid) {                             // one jump table (BRX) over every case
