@@ -138,7 +138,7 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   const int g_max = 128;
   pl.xsmem = eval_variant_s4().smem_bytes(g_max, S, n_cols, weighted, 1, predict) <=
              (size_t)kMaxDynSmem;
-  const int tile = pl.xsmem ? kTileSmem : kTile;
+  const int tile = pl.xsmem ? kTileSmem : kTileGlobal;
   const int64_t n_tiles = (n_rows + tile - 1) / tile;
   const int occ_guess = 4;
   // row-chunk items per resident CTA slot (tuning knob GP_ITEMS_PER_SLOT)
@@ -201,6 +201,13 @@ static gp_status launch_variants(gp_context* ctx, EvalArgs a, const EvalPlan& pl
       return ctx->fail(GP_ERR_ARG, "evaluator variant %d: wide shape SUB mismatch", v);
     a.stream = (const uint4*)ctx->codestream.p;
     a.item_order = pl.item_order;
+    // consecutive variant launches walk the row chunks in opposite directions, so each launch
+    // starts on the chunks the previous one left in L2 (C3: X + y = 201 MB vs 126 MB of L2)
+    static const bool env_rev = [] {                            // tuning knob GP_CHUNK_REVERSE
+      const char* e = getenv("GP_CHUNK_REVERSE");
+      return !e || atoi(e) != 0;
+    }();
+    a.chunk_reverse = env_rev ? (v & 1) : 0;
     a.gstart = (const int64_t*)ctx->gstart.p + (int64_t)v * (n + 1);
     a.prog_ids = (const int32_t*)ctx->lists.p + (int64_t)v * n;
     a.prog_count = (const int32_t*)ctx->counts.p + v;

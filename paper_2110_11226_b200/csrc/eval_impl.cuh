@@ -60,7 +60,7 @@ namespace GP_NS {
 constexpr int STACK = GP_STACK, R = GP_R, SUB = GP_SUB, NT = GP_NT;
 constexpr int TILE = NT * R * SUB;
 #ifdef GP_GLOBAL_X_ONLY
-static_assert(TILE == kTile, "wide-dataset shapes work on the 2048-row plan tile");
+static_assert(kTileGlobal % TILE == 0, "a wide-dataset shape's tile divides the plan tile");
 #else
 static_assert(TILE == kTileSmem, "shared-memory-X shapes stage the 8192-row plan tile");
 #endif
@@ -280,7 +280,8 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
     const int64_t item = s_item;
     if (item >= n_items) break;
     const int g = a.item_order ? (int)(item / a.n_chunks) : (int)(item % n_groups);
-    const int64_t q = a.item_order ? item % a.n_chunks : item / n_groups;
+    const int64_t q0 = a.item_order ? item % a.n_chunks : item / n_groups;
+    const int64_t q = a.chunk_reverse ? a.n_chunks - 1 - q0 : q0;
     const int np = min(Gv, count - g * Gv);
     const int32_t* __restrict__ gids = a.prog_ids + (int64_t)g * Gv;    // group's program ids
     const int64_t s_begin = a.gstart[g], s_len = a.gstart[g + 1] - s_begin;

@@ -11,9 +11,11 @@ namespace gpb {
 // kernel is variant independent): case id = opv * kCaseStride + slot.
 constexpr int kCaseStride = GP_MAX_STACK;
 // Row tiles (NT * R * SUB): the shared-memory-X shapes s4..s20 (512 threads) stage 8192-row
-// tiles; the wide-dataset shapes w4 / w8 (global-memory X) work on 2048-row tiles. Row chunks are
-// whole tiles of the plan's tile (kTileSmem when X is staged in shared memory, else kTile).
+// tiles; the wide-dataset shapes w4 / w8 (global-memory X) work on 4096- / 2048-row tiles. Row
+// chunks are whole tiles of the plan's tile: kTileSmem when X is staged in shared memory, else
+// kTileGlobal (every wide shape's tile divides it).
 constexpr int kTile = 2048;
+constexpr int kTileGlobal = 4096;
 constexpr int kTileSmem = 8192;
 // Dynamic shared-memory opt-in of the evaluator kernels (227 KB per CTA minus the kernels' 16 B of
 // static shared memory, rounded down).
@@ -64,6 +66,7 @@ struct EvalArgs {
   int64_t rows_per_chunk;     // rows per work item (whole plan tiles)
   int64_t n_chunks;           // row chunks; work items = ceil(count / G) * n_chunks
   int32_t item_order;         // work-item order: 0 = program group fastest, 1 = row chunk fastest
+  int32_t chunk_reverse;      // 1: row chunks are visited last to first (see launch_variants)
   double* partial;            // FIT: [n_chunks][ld_part], ld_part = kConstCols + n_programs * S
   int64_t ld_part;
   const int32_t* part_base;   // FIT, device: first compact partial slot of this variant's bucket

@@ -9,3 +9,6 @@
 #define GP_RED_ROWS 8
 #define GP_GLOBAL_X_ONLY 1
 
+// as shape_w4.h: sin * rcp(cos) tan and the shared case tail
+#define GP_TAN_POLY 0
+#define GP_CASE_CONTINUE 0

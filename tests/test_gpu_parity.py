@@ -23,6 +23,8 @@ FP32_SUM_LIMIT = float(np.finfo(np.float32).max) / 512
 # Tolerance model: DESIGN.md "Tolerance model" (north_star: relative 1e-4 in fp32).
 # row tile of the shared-memory-X evaluator shapes (kernels.h kTileSmem)
 SMEM_TILE = 8192
+# plan tile of the wide-dataset (global-memory X) shapes (kernels.h kTileGlobal)
+GLOBAL_TILE = 4096
 
 
 @pytest.fixture(scope="module")
@@ -198,9 +200,9 @@ def test_predict_deep_random_all_ops_stress(gp, ctx, orc):
 
 
 def test_predict_global_x_path(gp, ctx, orc):
-    # 28 columns x 2048-row tile exceeds the shared-memory X budget -> per-node L1/L2 loads
-    # (wide-data shapes w4 / w8: 256-thread CTAs, 8 / 4 rows per thread)
-    X, _ = synth.higgs_like(2048 * 2 + 301, seed=4)
+    # 28 columns x 8192-row tile exceeds the shared-memory budget -> per-node L1/L2 loads
+    # (wide-data shapes w4 / w8: 4096- / 2048-row tiles)
+    X, _ = synth.higgs_like(GLOBAL_TILE * 2 + 301, seed=4)
     nodes, off = synth.random_population(60, seed=9, depth=(1, 6), funcs=synth.ALL_FUNCS,
                                          n_features=28, max_stack=8)
     out, st = ctx.predict(dev(nodes), dev(off), dev(X), max_stack=8)
@@ -211,7 +213,7 @@ def test_predict_global_x_path(gp, ctx, orc):
 def test_predict_global_x_every_variant(gp, ctx, orc):
     """Left-deep programs needing 2..20 slots on a wide dataset: every global-X variant (w4, w8,
     s12, s20) runs, each with its own shape."""
-    X, _ = synth.higgs_like(2048 + 517, seed=6)
+    X, _ = synth.higgs_like(GLOBAL_TILE + 517, seed=6)
     dn, do = synth.deep_population(60, seed=21, need=(2, 20))
     dn = dn.copy()
     v = dn[:, 0] == synth.VAR
@@ -282,7 +284,7 @@ def test_evaluate_deep_variants(gp, ctx, orc, max_stack, metric):
 
 
 def test_evaluate_global_x_path_logloss(gp, ctx, orc):
-    X, y = synth.higgs_like(2048 * 3 + 5, seed=12)          # 28 columns -> global X path
+    X, y = synth.higgs_like(GLOBAL_TILE * 3 + 5, seed=12)   # 28 columns -> global X path
     nodes, off = synth.random_population(60, seed=13, depth=(1, 6), n_features=28, max_stack=8)
     w = synth.weights(X.shape[1], seed=2)
     fit, _ = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), dev(w), metric="logloss",
