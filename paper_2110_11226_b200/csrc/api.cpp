@@ -133,11 +133,30 @@ int gpb::sm_count(int device) {
 EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t n_cols, int S,
                         bool predict, bool weighted, int force_G, int64_t force_tpc) {
   EvalPlan pl;
-  // X is staged in shared memory when the s4 shape's whole layout fits at the largest group
+  // X is staged in shared memory when the s4 shape's whole layout fits at 128-program groups
   // (8192-row tiles, see kernels.h); otherwise the wide-dataset shapes read X through L1/L2
-  const int g_max = 128;
-  pl.xsmem = eval_variant_s4().smem_bytes(g_max, S, n_cols, weighted, 1, predict) <=
+  pl.xsmem = eval_variant_s4().smem_bytes(128, S, n_cols, weighted, 1, predict) <=
              (size_t)kMaxDynSmem;
+  // Largest program group: on the shared-memory path the largest of 512 / 256 / 128 whose
+  // accumulators still fit (each staged X / y tile then serves more programs: C3 step 121.7 ->
+  // 119.5 -> 118.1 ms at 128 / 256 / 512); 128 on the global-X path, where larger groups keep
+  // more distinct code streams' variable loads in flight per row chunk (C4 step 42.0 -> 50.7 ms
+  // at 256). Tuning knob GP_G_MAX caps it.
+  static const int env_gmax = [] {
+    const char* e = getenv("GP_G_MAX");
+    return e && atoi(e) > 0 ? std::min(atoi(e), 1024) : 0;
+  }();
+  int g_max = 128;
+  if (pl.xsmem) {
+    for (int g : {512, 256}) {
+      if (env_gmax > 0 && g > env_gmax) continue;
+      if (eval_variant_s4().smem_bytes(g, S, n_cols, weighted, 1, predict) <= (size_t)kMaxDynSmem) {
+        g_max = g;
+        break;
+      }
+    }
+  }
+  if (env_gmax > 0 && env_gmax < g_max) g_max = env_gmax;
   const int tile = pl.xsmem ? kTileSmem : kTileGlobal;
   const int64_t n_tiles = (n_rows + tile - 1) / tile;
   const int occ_guess = 4;
@@ -157,6 +176,13 @@ EvalPlan gpb::plan_eval(int device, int64_t n_rows, int32_t n_programs, int32_t 
   if (force_G > 0) G = std::min(force_G, g_max);               // gp_context_set_plan
   const int n_groups = (n_programs + G - 1) / G;
   int64_t Q = std::min<int64_t>(n_tiles, std::max<int64_t>(1, (slots * per_slot + n_groups - 1) / n_groups));
+  // the fp64 partial buffer (row chunks x evaluated programs x S) is written and tile-reduced
+  // every evaluation: at most GP_PARTIAL_MB (default 64) MB of it
+  static const int64_t part_mb = [] {
+    const char* e = getenv("GP_PARTIAL_MB");
+    return (int64_t)(e && atoi(e) > 0 ? atoi(e) : 64);
+  }();
+  Q = std::min<int64_t>(Q, std::max<int64_t>(1, (part_mb << 20) / ((int64_t)n_programs * S * 8)));
   int64_t tpc = (n_tiles + Q - 1) / Q;
   if (force_tpc > 0) tpc = std::min<int64_t>(force_tpc, n_tiles);
   Q = (n_tiles + tpc - 1) / tpc;
