@@ -67,6 +67,9 @@ LOSS_SFU = {"logloss": 2}
 # (profiles/pipe_peaks_r01.txt). FP32: 148 x 128 lanes x 1965 MHz.
 SFU_PEAK = 148 * 16 * 1965e6
 FP32_PEAK = 148 * 128 * 1965e6
+# L2 read bandwidth, measured: tools/l2_peak.cu (16-byte ld.global.cg loads of an L2-resident
+# buffer from every SM; profiles/l2_peak_r02.txt)
+L2_PEAK_GBS = 18548.6
 
 
 def load_dataset(cfg, rank=0, world=1):
@@ -144,8 +147,22 @@ def algorithmic_ops(op_count, rows, metric, n_programs, const_programs=0):
     return sfu, fp32
 
 
-def roofline_of(sfu, fp32, eval_ms, launches, step_ms, traffic=None):
-    """Binding ALU pipe of the evaluator for the given algorithmic work: SFU (MUFU) or FP32."""
+def l2_operands(var_nodes, rows, eval_ms):
+    """Wide datasets (X read through L1/L2): every variable operand of a
+    variable-dependent node is a 4-byte L2 read per row (no shared-memory X tile); achieved rate of
+    those reads against the measured L2 read bandwidth (tools/l2_peak.cu)."""
+    b = float(var_nodes) * rows * 4
+    gbs = b / (eval_ms * 1e-3) / 1e9
+    return {"bytes": b, "achieved": round(gbs, 1), "peak": L2_PEAK_GBS, "unit": "GB/s",
+            "frac": round(gbs / L2_PEAK_GBS, 4),
+            "note": "variable-operand reads (variable nodes x rows x 4 B) / eval time vs the "
+                    "measured L2 read bandwidth (profiles/l2_peak_r02.txt)"}
+
+
+def roofline_of(sfu, fp32, eval_ms, launches, step_ms, traffic=None, l2_var_nodes=None,
+                rows=None):
+    """Binding ALU pipe of the evaluator for the given algorithmic work: SFU (MUFU) or FP32; for
+    wide datasets also the L2 rate of the variable-operand reads (l2_var_nodes x rows)."""
     eval_s = eval_ms * 1e-3
     f_sfu, f_fp32 = sfu / eval_s / SFU_PEAK, fp32 / eval_s / FP32_PEAK
     if f_sfu >= f_fp32:
@@ -163,6 +180,8 @@ def roofline_of(sfu, fp32, eval_ms, launches, step_ms, traffic=None):
               "eval_share_of_step": round(eval_ms / step_ms, 4),
               "peak_note": "SFU: 148 SMs x 16 MUFU/clk x 1965 MHz (measured MUFU.SIN 4.63e12/s); "
                            "FP32: 148 x 128 x 1965 MHz"})
+    if l2_var_nodes is not None:
+        r["l2_operands"] = l2_operands(l2_var_nodes, rows, eval_ms)
     return r
 
 
@@ -322,7 +341,10 @@ def run_b200(args, cfg):
         a, b2 = algorithmic_ops(s["op_count"], rows_local, cfg["metric"], cfg["pop"],
                                 0 if args.no_const_programs else s["const_programs"])
         sfu, fp32 = sfu + a, fp32 + b2
-    roofline = roofline_of(sfu, fp32, eval_ms, eval_launches, ms, traffic=args.config)
+    wide = cfg["data"] != "pagie"            # X through L1/L2 (no shared-memory X tile)
+    roofline = roofline_of(sfu, fp32, eval_ms, eval_launches, ms, traffic=args.config,
+                           l2_var_nodes=sum(s["op_count"][0] for s in steps) if wide else None,
+                           rows=rows_local)
 
     # ---- gp_evaluate alone on the fixed generation-0 population (SURVEY D definition) -----------
     fit_buf = torch.empty(cfg["pop"], dtype=torch.float32, device=f"cuda:{local}")
@@ -346,7 +368,8 @@ def run_b200(args, cfg):
     t_med = statistics.median(times)
     a0_, b0_ = algorithmic_ops(st0["op_count"], rows_local, cfg["metric"], cfg["pop"],
                                0 if args.no_const_programs else st0["const_programs"])
-    roof0 = roofline_of(a0_ * reps, b0_ * reps, k_ms, k_l, k_ms)
+    roof0 = roofline_of(a0_ * reps, b0_ * reps, k_ms, k_l, k_ms,
+                        l2_var_nodes=st0["op_count"][0] * reps if wide else None, rows=rows_local)
     evaluate = {"population": "generation 0 (ramped half-and-half), mean length %.2f"
                               % (n0_len / cfg["pop"]),
                 "reps": reps, "median_ms": round(t_med, 3), "min_ms": round(min(times), 3),

@@ -171,8 +171,10 @@ gp_status gp_context_set_const_programs(gp_context* ctx, int closed_form);
 typedef enum { GP_SHARD_ROWS = 0, GP_SHARD_PROGRAMS = 1 } gp_shard;
 gp_status gp_context_set_shard(gp_context* ctx, gp_shard mode);
 /* Work decomposition override (tests and tuning): group_size programs per work item
- * (1..128, 0 = automatic) and tiles_per_chunk row tiles of 2048 rows per work item (0 =
- * automatic). Only the fp64 summation order of the per-chunk partial sums depends on it. */
+ * (1..512, 0 = automatic; capped to the largest group whose accumulators fit: 128 on the
+ * global-memory-X path) and tiles_per_chunk plan tiles per work item (8192 rows when X is staged
+ * in shared memory, 4096 otherwise; 0 = automatic). Only the fp64 summation order of the
+ * per-chunk partial sums depends on it. GP_ERR_ARG for values out of range. */
 gp_status gp_context_set_plan(gp_context* ctx, int32_t group_size, int64_t tiles_per_chunk);
 /* Restricts gp_evaluate / gp_evaluate_partial to the programs [lo, hi) (hi < 0: all) -- the
  * per-rank program chunk of GP_SHARD_PROGRAMS, usable without a communicator (a caller that

@@ -353,7 +353,7 @@ gp_status gp_context_set_stream(gp_context* ctx, void* stream) {
 }
 
 gp_status gp_context_set_plan(gp_context* ctx, int32_t group_size, int64_t tiles_per_chunk) {
-  if (!ctx || group_size < 0 || group_size > 128 || tiles_per_chunk < 0) return GP_ERR_ARG;
+  if (!ctx || group_size < 0 || group_size > 512 || tiles_per_chunk < 0) return GP_ERR_ARG;
   ctx->plan_G = group_size;
   ctx->plan_tpc = tiles_per_chunk;
   return GP_OK;

@@ -74,17 +74,22 @@ def _case(orc, cache, metric, weighted):
     return cache[key]
 
 
+@pytest.mark.parametrize("group", [128, 512])
 @pytest.mark.parametrize("weighted", [False, True])
 @pytest.mark.parametrize("metric", METRICS)
-def test_production_plan_every_program(gp, pctx, orc, oracle_cache, metric, weighted):
+def test_production_plan_every_program(gp, pctx, orc, oracle_cache, metric, weighted, group):
+    """group 128: the global-X path's and the r01 group size; 512: the shared-memory path's
+    largest group (C3 runs 512; the planner caps it to what fits: 256 for Pearson and weighted
+    losses), i.e. one group per bucket here -- 24 reduction-block flushes and a multi-window
+    stream per tile."""
     X, y, w, nodes, off, ref, sens, flags = _case(orc, oracle_cache, metric, weighted)
     assert X.shape[1] % 8192 != 0
-    pctx.set_plan(128, 3)                       # 128-program groups, 3-tile chunks (3 chunks)
+    pctx.set_plan(group, 3)                     # 3-tile chunks (3 chunks, the last ragged)
     fit, st = pctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), None if w is None else dev(w),
                             metric=metric, max_stack=8)
     torch.cuda.synchronize()
     check_fitness(fit.cpu().numpy(), ref, sens, flags, metric,
-                  label=f"production plan {metric} w={weighted}")
+                  label=f"production plan G={group} {metric} w={weighted}")
     # the automatic plan (small groups, one-tile items) agrees to summation order
     pctx.set_plan(0, 0)
     fa, sa = pctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), None if w is None else dev(w),

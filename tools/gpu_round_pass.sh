@@ -1,13 +1,15 @@
-# round-2 pass 2: full GPU suite, smoke, bench lines for every config, reference arm, launch list
-export GP_PARITY_LOG=gpurun_out/parity_counts.jsonl
+# round pass: full GPU suite, smoke, bench lines for every config, reference arm, launch list
+#   bash tools/gpu_round_pass.sh <tag>      (outputs gpurun_out/*_<tag>*)
+T=${1:-v4}
+export GP_PARITY_LOG=gpurun_out/parity_counts_$T.jsonl
 rm -f $GP_PARITY_LOG
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_t4.log 2>&1; echo pytest=$?
-tail -n 6 gpurun_out/pytest_t4.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_t4.log 2>&1; echo smoke=$?; tail -n 2 gpurun_out/smoke_t4.log
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_$T.log 2>&1; echo pytest=$?
+tail -n 3 gpurun_out/pytest_$T.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$T.log 2>&1; echo smoke=$?; tail -n 2 gpurun_out/smoke_$T.log
 for c in c3 c2 c4 c5; do
-  timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/bench_t4_$c.log 2>&1; echo bench_$c=$?
-  tail -n 1 gpurun_out/bench_t4_$c.log > gpurun_out/bench_r02_v2_$c.json
+  timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/bench_${T}_$c.log 2>&1; echo bench_$c=$?
+  tail -n 1 gpurun_out/bench_${T}_$c.log > gpurun_out/bench_r02_${T}_$c.json
 done
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_t4_ref.log 2>&1; echo ref=$?
-tail -n 1 gpurun_out/bench_t4_ref.log > gpurun_out/bench_r02_v2_reference.json
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r02_v2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-evolved --eval-reps 10 > gpurun_out/ncu_launch_v2.log 2>&1; echo ncu=$?
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_${T}_ref.log 2>&1; echo ref=$?
+tail -n 1 gpurun_out/bench_${T}_ref.log > gpurun_out/bench_r02_${T}_reference.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r02_$T.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-evolved --eval-reps 10 > gpurun_out/ncu_launch_$T.log 2>&1; echo ncu=$?

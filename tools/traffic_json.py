@@ -29,13 +29,13 @@ for _, d in sorted(data.items()):
             d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0))
 n_eval = max(len(v) for v in per.values())
 out = {"source": f"{src} (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
-                 "gpu__time_duration.sum --clock-control none, every launch of `python bench.py "
+                 "gpu__time_duration.sum --clock-control none --cache-control none, every launch of `python bench.py "
                  "--steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-evolved`, config " + cfg + ")",
        "evaluations": n_eval,
        "per_variant_bytes_per_evaluation": {k: sum(v) / n_eval for k, v in per.items()},
        "algorithmic_bytes_per_evaluation": alg,
        "note": "one evaluation = one launch per non-empty stack-need variant; reads of X, y "
-               "plus the fp64 partial-sum writes; ncu flushes caches between launches",
+               "plus the fp64 partial-sum writes; caches are not flushed between launches (--cache-control none), as in a bench run",
        "dram_bytes_per_launch": sum(sum(v) for v in per.values()) / n_eval}
 json.dump(out, open(f"profiles/eval_kernel_ncu_{cfg}.json", "w"), indent=1)
 print(json.dumps(out["per_variant_bytes_per_evaluation"]), out["dram_bytes_per_launch"])
