@@ -231,6 +231,34 @@ inline size_t smem_total(int G, int S, int n_cols, bool weighted, bool xsmem, bo
 
 template <int M> struct MTag { static constexpr int value = M; };
 
+// TMA bulk copies (non-tensor) into shared memory, completion tracked by an mbarrier
+#ifndef GP_TMA_X
+#define GP_TMA_X 1
+#endif
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n\t.reg .pred p;\n"
+               "GP_WAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+               "@!p bra GP_WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// dst, src 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void tma_bulk_g2s(float* dst, const float* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ float warp_sum_f32(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -248,12 +276,22 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
     eval_kernel(const EvalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_item;
+  // shared-memory X tiles arrive by TMA bulk copies (cp.async.bulk) signalled on this mbarrier
+  __shared__ __align__(8) uint64_t s_xbar;
+  __shared__ uint32_t s_xphase;     // the mbarrier's current phase (thread 0 only)
   const int S = (a.metric == GP_PEARSON) ? 3 : 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int count = *a.prog_count;                 // programs in this variant's bucket
   // this bucket's group size (<= a.G; bucket_kernel), read once through shared memory
   __shared__ int s_gv;
-  if (threadIdx.x == 0) s_gv = *a.group_size;
+  if (threadIdx.x == 0) {
+    s_gv = *a.group_size;
+    if constexpr (XSMEM && GP_TMA_X) {
+      mbar_init(&s_xbar, 1);
+      s_xphase = 0;
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
   __syncthreads();
   const int Gv = s_gv;
   const int n_groups = (count + Gv - 1) / Gv;
@@ -295,6 +333,19 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
       const int nvalid = (int)min((int64_t)TILE, r_end - t0);
       __syncthreads();  // previous tile's smem reads are done
       // ---- A2: stage the tile (coalesced; padded rows get w = 0 -> skipped) -----------------
+      // X columns: one elected thread issues a TMA bulk copy per column (16-byte aligned
+      // columns, whole 16-byte rows; padded rows keep stale values: every use of a padded row is
+      // masked by w = 0 / the nvalid predicate); otherwise the threads copy, zero-padded
+      const bool tma_x = XSMEM && GP_TMA_X && x_vec && (nvalid & 3) == 0;
+      if constexpr (XSMEM && GP_TMA_X) {
+        if (tma_x && tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> async writes
+          mbar_expect_tx(&s_xbar, (uint32_t)(a.n_cols * nvalid * 4));
+          for (int c = 0; c < a.n_cols; ++c)
+            tma_bulk_g2s(xs + c * TILE, a.X + (int64_t)c * a.ldx + t0, (uint32_t)(nvalid * 4),
+                         &s_xbar);
+        }
+      }
       for (int i = tid; i < TILE; i += NT) {
         const bool in = i < nvalid;
         const int64_t row = t0 + i;
@@ -306,8 +357,17 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
           if (has_w) ws[i] = in ? a.w[row] : 0.0f;
         }
         if constexpr (XSMEM) {
-          for (int c = 0; c < a.n_cols; ++c)
-            xs[c * TILE + i] = in ? a.X[(int64_t)c * a.ldx + row] : 0.0f;
+          if (!tma_x)
+            for (int c = 0; c < a.n_cols; ++c)
+              xs[c * TILE + i] = in ? a.X[(int64_t)c * a.ldx + row] : 0.0f;
+        }
+      }
+      if constexpr (XSMEM && GP_TMA_X) {
+        // thread 0 waits for the X bytes, the barrier releases everyone (no phase register is
+        // kept live through the hot loop below)
+        if (tma_x && tid == 0) {
+          mbar_wait_parity(&s_xbar, s_xphase);
+          s_xphase ^= 1u;
         }
       }
       __syncthreads();
