@@ -1,13 +1,16 @@
 // eval_impl.cuh -- the fused population evaluator, sm_100a.
 //
-// Included by eval_s{4,8,12,20}.cu with GP_STACK (register-stack capacity), GP_R (rows per thread
-// per pass), GP_SUB (passes per program per tile), GP_NT (threads per CTA) and GP_MINB (resident
-// CTAs per SM the register budget must allow) defined, so every (op, operand variant, slot) case of
-// the dispatch switch is generated for exactly GP_STACK slots.
+// Included by the translation units build.py generates from shape_<name>.h, which defines GP_STACK
+// (register-stack capacity), GP_R (rows per thread per pass), GP_SUB (passes per program per tile),
+// GP_NT (threads per CTA) and GP_MINB (resident CTAs per SM the register budget must allow), so
+// every (op, operand variant, slot) case of the dispatch switch is generated for exactly GP_STACK
+// slots. Shared-memory-X shapes run one 512-thread CTA per SM (the warps of an SM sub-partition
+// share the instruction cache while they walk the same code stream).
 //
 // Persistent CTAs pull work items (program group g x row chunk q) from a queue. Per item:
-//   for each tile of TILE = NT*R*SUB = 2048 rows of the chunk:
-//     stage y, w (and X when n_cols is small) into shared memory, coalesced, zero-padded  [A2]
+//   for each tile of TILE = NT*R*SUB rows of the chunk (8192; wide shapes 4096 / 2048):
+//     stage the tile into shared memory: X (when the layout fits) by TMA bulk copies on an
+//     mbarrier, y / w by the threads, coalesced, zero-padded                            [A2]
 //     walk the group's packed code stream (aux.cu pack_kernel): for each program of the group
 //     (programs of this variant's stack-need bucket), SUB copies of its code, one per row pass,
 //     the last word of each pass flagged so the loss / reduction follows its case -- one
@@ -19,7 +22,8 @@
 //         node dispatches an (op, operand-source, slot) case; no stack index is ever computed at
 //         run time (the paper's unrolled slot loop, costs O(capacity) per push) [A3]
 //       fused weighted loss of those rows (no m x n prediction matrix)             [A4]
-//       warp shuffle reduction, lane 0 accumulates into a per-(warp, program) fp64 smem slot   [A5]
+//       per-lane fp32 sums -> the warp's 16-program shared-memory reduction block -> fp64
+//       per-(warp, program) accumulators (Pearson: warp shuffles)                            [A5]
 //   per-program sums over warps in fixed order -> partial[q][bucket position] (no atomics on data:
 //   the sums do not depend on which CTA ran which item)
 //
