@@ -1,11 +1,13 @@
 // Evaluator variant for wide datasets: register stack of 8 slots, 4 rows per thread, 2 passes per
-// tile, 256-thread CTAs at an 80-register budget (see eval_w4.cu).
+// tile (4096 rows), 512-thread CTAs at a 64-register budget (2 CTAs = 32 warps per SM; r02 A/B:
+// 256 threads at 80 registers, 24 warps, C5 gp_evaluate 37.1 ms -> 35.0 ms here,
+// profiles/ab_r02_wide_shapes3.log).
 #define GP_STACK 8
 #define GP_R 4
 #define GP_SUB 2
-#define GP_NT 256
-#define GP_MINB 3
-#define GP_MINB_GLOBAL 3
+#define GP_NT 512
+#define GP_MINB 2
+#define GP_MINB_GLOBAL 2
 #define GP_RED_ROWS 8
 #define GP_GLOBAL_X_ONLY 1
 
