@@ -268,6 +268,36 @@ def test_evaluate_fitness_matches_oracle(gp, ctx, orc, metric, weighted):
     check_fitness(fit.cpu().numpy(), ref, sens, flags, metric)
 
 
+@pytest.mark.parametrize("metric", ["mse", "mae", "pearson"])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_tma_and_thread_staging_agree(gp, ctx, orc, metric, weighted):
+    """The shared-memory X tile arrives by TMA bulk copies when every column is 16-byte aligned and
+    the tile's row count is a multiple of 4 (padded rows keep the previous tile's values, masked by
+    the row predicate), else by the threads with zero padding (DESIGN.md section 8 item 0). The
+    same data through both paths -- contiguous X vs a view with a 9,217-float column stride; a
+    ragged last tile of 1,024 rows -- gives bit-identical fitness, and matches the oracle."""
+    X, y = synth.pagie_grid(96)                      # 9,216 rows = one 8192-row tile + 1,024
+    n = X.shape[1]
+    assert (n - 8192) % 4 == 0
+    nodes, off = synth.random_population(200, seed=17 + len(metric), depth=(0, 6), max_stack=8)
+    w = synth.weights(n, seed=9) if weighted else None
+    wd = None if w is None else dev(w)
+    fit_tma, st_tma = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), wd, metric=metric,
+                                   max_stack=8)
+    Xb = torch.zeros((X.shape[0], n + 1), dtype=torch.float32, device="cuda")
+    Xb[:, :n] = dev(X)
+    Xv = Xb[:, :n]                                   # ldx = n + 1: unaligned columns, thread path
+    assert Xv.stride(0) % 4 != 0
+    fit_thr, st_thr = ctx.evaluate(dev(nodes), dev(off), Xv, dev(y), wd, metric=metric,
+                                   max_stack=8)
+    torch.cuda.synchronize()
+    assert torch.equal(st_tma, st_thr)
+    a, b = fit_tma.cpu().numpy(), fit_thr.cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    ref, sens, flags = orc.population_fitness(nodes, off, X, y, w, metric)
+    check_fitness(a, ref, sens, flags, metric, label=f"tma staging {metric} w={weighted}")
+
+
 @pytest.mark.parametrize("max_stack", [12, 20])
 @pytest.mark.parametrize("metric", ["mse", "pearson"])
 def test_evaluate_deep_variants(gp, ctx, orc, max_stack, metric):
