@@ -66,7 +66,7 @@ constexpr int TILE = NT * R * SUB;
 #ifdef GP_GLOBAL_X_ONLY
 static_assert(kTileGlobal % TILE == 0, "a wide-dataset shape's tile divides the plan tile");
 #else
-static_assert(TILE == kTileSmem, "shared-memory-X shapes stage the 8192-row plan tile");
+static_assert(kTileSmem % TILE == 0, "a shared-memory-X shape's tile divides the plan tile");
 #endif
 constexpr int NW = NT / 32, R4 = R / 4;
 constexpr int RR = GP_RED_ROWS, LPR = 32 / RR, RED_BYTES = NW * RR * kRedStride * 4;

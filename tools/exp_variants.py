@@ -34,7 +34,9 @@ def one(var, name, shape):
     defs += "".join(f"#define {kv.split(':')[0]} {kv.split(':')[1]}\n" for kv in extra)
     exp = os.path.join(PKG, "_exp")
     os.makedirs(exp, exist_ok=True)
-    modes = [(0, 0), (1, 0)] if var.startswith("w") else [(0, 0), (0, 1), (1, 0), (1, 1)]
+    m = B.SHAPES[var]                     # the shape's build modes (build.py)
+    modes = ([(0, 0), (1, 0)] if m == "P" else [(0, 1), (1, 1)] if m == "S"
+             else [(0, 0), (0, 1), (1, 0), (1, 1)])
     objs = []
     impl = os.path.join(PKG, "csrc", "eval_impl.cuh")
 
