@@ -103,7 +103,8 @@ inline size_t smem_total(int G, int S, int n_cols, bool weighted, bool xsmem, bo
 // with the next dispatch straight from the case (one taken branch per word instead of two: case ->
 // shared tail -> loop head); C3 step 123.2 -> 121.2 ms (profiles/ab_r02_dispatch.log). The
 // compiled loop head then also rotates the two prefetched case ids without waiting on the LDS.
-// (GP_PREFETCH = 1, a one-deep id prefetch, was measured slower: 125.5 ms.)
+// (GP_PREFETCH = 1, a one-deep id prefetch, measured slower without the per-case continue,
+// 125.5 ms, and slightly faster with it on the final build: shape_s4.h sets it.)
 #ifndef GP_CASE_CONTINUE
 #define GP_CASE_CONTINUE 1
 #endif

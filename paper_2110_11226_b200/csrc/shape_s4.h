@@ -8,3 +8,6 @@
 #define GP_SUB 1
 #define GP_NT 512
 #define GP_MINB 1
+// one-deep case-id prefetch (r02 A/B on the final build: gen-0 gp_evaluate 181.3 -> 178.6 ms,
+// step 118.0 -> 117.8 ms; it was slower before the per-case continue, profiles/ab_r02_s4misc.log)
+#define GP_PREFETCH 1
