@@ -22,3 +22,6 @@
 // 15.1 -> 14.0 ms without the per-case continue).
 #define GP_TAN_POLY 0
 #define GP_CASE_CONTINUE 0
+// one-deep case-id prefetch (as shape_s4.h; C4 step 39.7 -> 39.5 ms, C5 12.12 -> 12.06 ms,
+// profiles/ab_r02_s4misc.log)
+#define GP_PREFETCH 1
