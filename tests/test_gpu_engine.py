@@ -96,7 +96,7 @@ def test_full_size_c3_sampled(gp, ctx, orc):
     nodes, off, fit = e.population()
     rng = np.random.default_rng(0)
     lens = np.diff(off)
-    sample = list(rng.choice(np.where(lens > 5)[0], 3, replace=False)) + [int(np.argmax(lens))]
+    sample = list(rng.choice(np.where(lens > 5)[0], 11, replace=False)) + [int(np.argmax(lens))]
     sub_nodes = np.concatenate([nodes[off[p]:off[p + 1]] for p in sample])
     sub_off = np.zeros(len(sample) + 1, np.int64)
     sub_off[1:] = np.cumsum([lens[p] for p in sample])
@@ -105,7 +105,7 @@ def test_full_size_c3_sampled(gp, ctx, orc):
 
 
 def test_full_size_c3_decomposition_invariant(gp, ctx):
-    """Every program of the C3 population at full size (bench launch configuration: groups of 128
+    """Every program of the C3 population at full size (bench launch configuration: groups of 512
     programs whose code streams span several shared-memory windows, 16-program reduction blocks)
     against the same programs evaluated 8 at a time (groups of 8, one window): the work
     decomposition only changes the fp32 / fp64 summation order. Constant programs are compared
