@@ -351,6 +351,24 @@ def full_tree(orc, depth):
     return np.concatenate([orc.program("add"), sub, sub])
 
 
+@pytest.mark.parametrize("m,d", [(3, 1), (255, 1), (4099, 90), (1000, 2000)])
+@pytest.mark.parametrize("metric", ["mse", "pearson"])
+def test_dataset_shapes(gp, ctx, orc, m, d, metric):
+    """SURVEY section 4's shape grid: tiny row counts (one partial tile, a few live rows per warp),
+    a single column (shared-memory X), 90 columns (global X) and 2,000 columns (variable indices up
+    to 1,999, column offsets beyond 2^21 floats), weighted with zeros; every program vs the oracle."""
+    X = np.random.default_rng(m + d).standard_normal((d, m), dtype=np.float32)
+    y = (X[0] * X[d - 1] + np.sin(X[d // 2])).astype(np.float32)
+    w = synth.weights(m, seed=d)
+    nodes, off = synth.random_population(120, seed=m + 3 * d, depth=(0, 5), n_features=d,
+                                         max_stack=8)
+    fit, st = ctx.evaluate(dev(nodes), dev(off), dev(X), dev(y), dev(w), metric=metric,
+                           max_stack=8)
+    torch.cuda.synchronize()
+    ref, sens, flags = orc.population_fitness(nodes, off, X, y, w, metric)
+    check_fitness(fit.cpu().numpy(), ref, sens, flags, metric, label=f"shape m={m} d={d}")
+
+
 def test_edge_cases(gp, ctx, orc):
     P = orc.program
     progs = [
