@@ -179,7 +179,10 @@ def roofline_of(sfu, fp32, eval_ms, launches, step_ms, traffic=None, l2_var_node
               "eval_ms_per_launch": round(eval_ms / max(launches, 1), 3),
               "eval_share_of_step": round(eval_ms / step_ms, 4),
               "peak_note": "SFU: 148 SMs x 16 MUFU/clk x 1965 MHz (measured MUFU.SIN 4.63e12/s); "
-                           "FP32: 148 x 128 x 1965 MHz"})
+                           "FP32: 148 x 128 x 1965 MHz",
+              "work_note": "per-row work of variable-dependent nodes only; tan = 1 SFU op (range "
+                           "reduction + polynomial + one reciprocal, 13 FP32 ops; r01 counted 3: "
+                           "sin, cos, rcp), DESIGN.md section 8"})
     if l2_var_nodes is not None:
         r["l2_operands"] = l2_operands(l2_var_nodes, rows, eval_ms)
     return r
