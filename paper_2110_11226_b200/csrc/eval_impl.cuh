@@ -122,6 +122,7 @@ inline size_t smem_total(int G, int S, int n_cols, bool weighted, bool xsmem, bo
 // the tile.
 #define GP_VAR4(v, var, k)                                                                     \
   float4 v;                                                                                    \
+  GP_CHECK((int)(var) >= 0 && (int)(var) < a.n_cols);                                          \
   if constexpr (XSMEM) {                                                                       \
     v = reinterpret_cast<const float4*>(xs + (int)(var) * TILE + ebase)[(k) * NT];             \
   } else {                                                                                     \
@@ -237,6 +238,18 @@ inline size_t smem_total(int G, int S, int n_cols, bool weighted, bool xsmem, bo
 
 template <int M> struct MTag { static constexpr int value = M; };
 
+// GP_DEBUG_BOUNDS (build.py GP_BUILD_DEBUG=1): every index into the code stream, the shared-memory
+// tiles, the accumulators and the partial buffer is checked; a violation traps (the launch fails
+// with an error). Off in the product build.
+#ifndef GP_DEBUG_BOUNDS
+#define GP_DEBUG_BOUNDS 0
+#endif
+#if GP_DEBUG_BOUNDS
+#define GP_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define GP_CHECK(cond) do { } while (0)
+#endif
+
 // TMA bulk copies (non-tensor) into shared memory, completion tracked by an mbarrier
 #ifndef GP_TMA_X
 #define GP_TMA_X 1
@@ -326,6 +339,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
     const int g = a.item_order ? (int)(item / a.n_chunks) : (int)(item % n_groups);
     const int64_t q0 = a.item_order ? item % a.n_chunks : item / n_groups;
     const int64_t q = a.chunk_reverse ? a.n_chunks - 1 - q0 : q0;
+    GP_CHECK(g >= 0 && g < n_groups && q >= 0 && q < a.n_chunks);
     const int np = min(Gv, count - g * Gv);
     const int32_t* __restrict__ gids = a.prog_ids + (int64_t)g * Gv;    // group's program ids
     const int64_t s_begin = a.gstart[g], s_len = a.gstart[g + 1] - s_begin;
@@ -344,6 +358,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
       // masked by w = 0 / the nvalid predicate); otherwise the threads copy, zero-padded
       const bool tma_x = XSMEM && GP_TMA_X && x_vec && (nvalid & 3) == 0;
       if constexpr (XSMEM && GP_TMA_X) {
+        GP_CHECK(!tma_x || (int64_t)a.n_cols * nvalid * 4 < (1 << 20));   // mbarrier tx count
         if (tma_x && tid == 0) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> async writes
           mbar_expect_tx(&s_xbar, (uint32_t)(a.n_cols * nvalid * 4));
@@ -404,6 +419,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
         }
 #pragma unroll
         for (int o = 1; o < LPR; o <<= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+        GP_CHECK(p0 >= 0 && p0 + n <= a.G && n <= RR);
         if (part == 0 && row < n) acc[(size_t)warp * a.G + p0 + row] += (double)m;
         __syncwarp();
       };
@@ -525,6 +541,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
         const int wn = (int)min((int64_t)kStreamWin, s_len - w0);
         if (s_len > kStreamWin || t0 == r_begin) {
           __syncthreads();                           // every warp is done with the old window
+          GP_CHECK(wn > 0 && wn <= kStreamWin);
           for (int i = tid; i < wn + 2; i += NT) sw[i] = __ldg(a.stream + s_begin + w0 + i);
           __syncthreads();
         }
@@ -552,6 +569,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
 #endif
           const uint4 cw = *wp;
           ++wp;
+          GP_CHECK(wp <= sw + kStreamWin);             // never past the window's last word
           switch (cid) {                             // one jump table (BRX) over every case
             GP_ALL_CASES
             default: __builtin_unreachable();        // stage / pack guarantee a valid case
@@ -564,6 +582,7 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
               } else {                               // program done (A5)
                 if constexpr (!PREDICT) {
                   const int j = (int)(cw.w >> 8);    // == pslot
+                  GP_CHECK(j == pslot && j < np && j < a.G);
                   if (S == 1) {
                     rbw[(j % RR) * kRedStride + lane] = l0 + l1;  // l1: odd rows (MSE)
                     if (j % RR == RR - 1) flush(j - (RR - 1), RR);
@@ -594,6 +613,8 @@ __global__ void __launch_bounds__(NT, XSMEM ? GP_MINB : GP_MINB_GLOBAL)
       // only programs that were evaluated per row are written and tile-reduced
       double* prow = a.partial + q * a.ld_part + kConstCols +
                      ((int64_t)*a.part_base + (int64_t)g * Gv) * S;
+      GP_CHECK(np >= 0 && np <= Gv && Gv <= a.G &&
+               kConstCols + ((int64_t)*a.part_base + (int64_t)g * Gv + np) * S <= a.ld_part);
       for (int j = tid; j < np * S; j += NT) {
         const int pl = j / S, k = j - pl * S;
         double sum = 0.0;
